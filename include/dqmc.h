@@ -1,0 +1,122 @@
+/*
+ * dqmc.h — C ABI of the B200-native dense prime-implicant engine (libdqmc.so).
+ *
+ * Drop-in boundary for the reference's dense path. Every entry point below
+ * replaces a reference interface (paths relative to /root/reference/pkg):
+ *
+ *   dqmc_primes_tt / dqmc_primes_u8
+ *       replace dense_prime_ranks(tt, h, optimized, mem_cap)
+ *       src/implicants/dense.py:405-418, reached through
+ *       run_engine("dense", ...) src/implicants/bench.py:94-108.
+ *       Output contract: caller-owned int64 ranks, unique, ascending
+ *       (dense.py:395-397); empty result = count 0.
+ *   dqmc_state_bytes
+ *       replaces state_bytes(n, h) src/implicants/dense.py:61-63.
+ *   DQMC_ERR_RESOURCE + dqmc_last_error()
+ *       replaces ResourceLimitError raised by load() before allocating,
+ *       message naming the needed byte count (dense.py:358-364,
+ *       errors.py:23-24).
+ *   DQMC_ERR_INVALID
+ *       replaces ValueError for a bad split h (dense.py:356-357) or n.
+ *   dqmc_state_device / dqmc_state_download
+ *       expose the final bitmap in DenseState.words layout (h = 5,
+ *       dense.py:127-170) for bitmap-level parity and k-GPU checks.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in signatures
+ * (streams are passed as void*; NULL = the library's own stream).
+ * All host-buffer entry points are synchronous: results are complete on
+ * return, as the reference's Python call is (SURVEY.md §8(b) "Threading").
+ */
+#ifndef DQMC_H
+#define DQMC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DQMC_ABI_VERSION 1
+
+/* status codes */
+#define DQMC_OK 0
+#define DQMC_ERR_INVALID 1  /* bad argument          -> ValueError          */
+#define DQMC_ERR_RESOURCE 2 /* memory cap exceeded    -> ResourceLimitError  */
+#define DQMC_ERR_CUDA 3     /* CUDA runtime failure                         */
+#define DQMC_ERR_NODEVICE 4 /* no CUDA device: fail loudly, never fall back */
+
+/* flags */
+#define DQMC_FLAG_KEEP_BITMAP 1u /* leave the final prime bitmap in the device state */
+#define DQMC_FLAG_TIMING 2u      /* record per-pass CUDA-event times (dqmc_last_timings) */
+#define DQMC_FLAG_COUNT_ONLY 4u  /* count primes, do not materialise ranks */
+
+/* input encodings */
+#define DQMC_IN_WORDS 0 /* TruthTable.words: max(1, 2^n/64) LE uint64, bit x = f(x) */
+#define DQMC_IN_U8 1    /* 2^n uint8 values, 0 = off, 1 = on, 2 = don't care (on ∪ dc) */
+
+typedef struct dqmc_result {
+    int64_t count;  /* number of prime implicants */
+    int64_t *ranks; /* host, ascending, count entries (NULL if count == 0 or COUNT_ONLY) */
+    void *_owner;   /* library bookkeeping; release with dqmc_free_result */
+} dqmc_result_t;
+
+int dqmc_abi_version(void);
+const char *dqmc_last_error(void);
+int dqmc_device_count(void);
+int dqmc_set_device(int device);
+
+/* dense.py:56-63 */
+uint64_t dqmc_block_bits(int h);
+uint64_t dqmc_state_bytes(int n, int h);
+
+/* Bytes the engine allocates on the device for n variables (state + scratch,
+ * excluding the rank output buffer). */
+uint64_t dqmc_device_bytes(int n);
+
+/* dense_prime_ranks(tt, h, optimized, mem_cap) from HOST buffers.
+ * h <= 0 means the default min(n, 5); mem_cap == 0 means 75% of free device
+ * memory. The result is independent of h and optimized (dense.py:405-418,
+ * tests/test_dense.py:218-229); both are validated exactly as the reference. */
+int dqmc_primes_tt(const uint64_t *tt_words, int n, int h, uint64_t mem_cap, uint32_t flags,
+                   dqmc_result_t *out);
+int dqmc_primes_u8(const uint8_t *values, int n, int h, uint64_t mem_cap, uint32_t flags,
+                   dqmc_result_t *out);
+void dqmc_free_result(dqmc_result_t *res);
+
+/* Same computation with DEVICE-resident input and output (bench `value`,
+ * torch integration). ranks_dev may be NULL (count only). If the count
+ * exceeds ranks_cap, *count_out is the true count and nothing beyond
+ * ranks_cap is written (DQMC_ERR_RESOURCE is NOT raised; the caller grows
+ * its buffer and calls again). Synchronises the stream to read the count. */
+int dqmc_primes_device(const void *input_dev, int in_kind, int n, int64_t *ranks_dev, int64_t ranks_cap,
+                       int64_t *count_out, uint32_t flags, void *stream);
+
+/* Per-pass timings of the last call made with DQMC_FLAG_TIMING. Returns the
+ * number of passes; fills up to max entries of kernel names and ms. */
+int dqmc_last_timings(const char **names, float *ms, int max);
+/* Algorithmic bytes (reads + writes the plan must do) of each timed pass. */
+int dqmc_last_pass_bytes(uint64_t *bytes, int max);
+
+/* Device pointer of the engine's state (reference layout, h = 5) after a
+ * call with DQMC_FLAG_KEEP_BITMAP, and its size in bytes. */
+int dqmc_state_device(void **ptr, uint64_t *bytes);
+
+/* Copy the device state to a host buffer of dqmc_state_bytes(n, 5) bytes. */
+int dqmc_state_download(void *host, uint64_t bytes);
+
+/* Device-side synthetic inputs (frozen generator of ttio.py:331-378 and the
+ * survey's 3-way / S-box variants); writes 2^n uint8. */
+int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint64_t seed, void *stream);
+
+/* The pass plan the engine runs for n variables (host logic, no GPU needed):
+ * out = {ne, H, g, T, m, r[0..7], a[0..7], ib_C, ib_E, ib_D[0..7], rank_sub}
+ * (32 int64 entries). Returns the number written. */
+int dqmc_plan(int n, int64_t *out, int max);
+
+/* Release all cached device/host workspaces. */
+void dqmc_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DQMC_H */

@@ -1,0 +1,64 @@
+"""B200-native dense Quine-McCluskey prime-implicant engine (arXiv 2302.10083).
+
+Drop-in for the reference's dense path (implicants.dense_prime_ranks /
+find_primes_dense, /root/reference/pkg/src/implicants/dense.py:405-428): same
+signature, int64 ascending ranks, same errors; the work runs in hand-written
+sm_100a kernels behind the C ABI of include/dqmc.h (libdqmc.so).
+"""
+
+from .dense import (
+    DEFAULT_SPLIT,
+    MERGE,
+    REDUCE,
+    block_bits_for,
+    count_primes,
+    dense_prime_ranks,
+    find_primes_dense,
+    prime_bitmap,
+    prime_ranks_from_values,
+    state_bytes,
+)
+from .engine import ENGINES, run_engine
+from .errors import ImplicantsError, ParseError, ResourceLimitError
+from .ternary import (
+    MAX_N,
+    SYMBOLS,
+    TruthTable,
+    index_to_rank,
+    rank,
+    rank_digits,
+    rank_weights,
+    ranks_to_text,
+    unrank,
+    unrank_many,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DEFAULT_SPLIT",
+    "ENGINES",
+    "ImplicantsError",
+    "MAX_N",
+    "MERGE",
+    "ParseError",
+    "REDUCE",
+    "ResourceLimitError",
+    "SYMBOLS",
+    "TruthTable",
+    "block_bits_for",
+    "count_primes",
+    "dense_prime_ranks",
+    "find_primes_dense",
+    "index_to_rank",
+    "prime_bitmap",
+    "prime_ranks_from_values",
+    "rank",
+    "rank_digits",
+    "rank_weights",
+    "ranks_to_text",
+    "run_engine",
+    "state_bytes",
+    "unrank",
+    "unrank_many",
+]

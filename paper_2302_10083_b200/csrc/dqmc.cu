@@ -1,0 +1,1120 @@
+// dqmc.cu — B200 (sm_100a) dense prime-implicant engine + C ABI (include/dqmc.h).
+//
+// Replaces the reference dense path (/root/reference/pkg/src/implicants/
+// dense.py:340-418): load -> MERGE all dims -> REDUCE all dims -> extract.
+// Design: the 3^(n-5) blocks of the reference layout are
+// swept in a handful of HBM passes instead of the reference's 2(n-5)+1:
+//
+//   pass A  k_c0_merge   : truth table -> blocks, in-block MERGE + the C0
+//                          block axes (contiguous 3^g-block tiles in smem);
+//                          only top-binary tiles are produced.
+//   pass B  k_strided<MERGE_ONLY>  : one group of <= 6 higher block axes,
+//                          reads the group's binary rows, writes its star rows.
+//   pass C  k_strided<MERGE_REDUCE>: last group: MERGE then REDUCE of the
+//                          group (+ some in-block axes); writes every block.
+//   pass D  k_strided<REDUCE>      : REDUCE of the remaining groups.
+//   pass E  k_c0_final   : REDUCE of the C0 axes + remaining in-block axes,
+//                          warp-aggregated popcount, decoupled look-back scan
+//                          and ordered compaction to int64 ranks.
+// Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dqmc.h"
+#include "dqmc_device.cuh"
+
+using namespace dqmc;
+
+namespace {
+
+constexpr int kC0Max = 7;        // block axes in the contiguous tile (3^7 blocks = 68.3 KiB)
+constexpr int kGroupMax = 6;     // block axes per strided pass (3^6 rows x 128 B = 91 KiB)
+constexpr int kRowBlocks = 4;    // blocks per strided row (128 B)
+constexpr int kStridedThreads = 288;  // 9 warps: 27 sub-cube tasks per round divide evenly
+constexpr int kTileThreads = 256;
+
+enum Mode { MERGE_ONLY = 0, MERGE_REDUCE = 1, REDUCE_ONLY = 2 };
+
+__host__ __device__ inline int64_t pow3l(int k) {
+    int64_t r = 1;
+    for (int i = 0; i < k; i++) r *= 3;
+    return r;
+}
+
+__device__ __forceinline__ int64_t bin_to_tern_rt(uint64_t b) {
+    int64_t r = 0, p = 1;
+    while (b) {
+        if (b & 1) r += p;
+        b >>= 1;
+        p *= 3;
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// input conversion
+
+// DQMC_IN_U8 -> 32-bit truth-table words (on ∪ dc, ternary.py:210-218), n >= 5
+__global__ void k_u8_to_words(const uint8_t *__restrict__ v, uint32_t *__restrict__ out, int64_t nwords) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = warp; w < nwords; w += nwarps) {
+        const unsigned bits = __ballot_sync(0xffffffffu, v[w * 32 + lane] != 0);
+        if (lane == 0) out[w] = bits;
+    }
+}
+
+// n < 5: pad with dummy variables n+1..5 (primes of f' = primes of f with '*'
+// appended, rank shifted by 3^5 - 3^n): the 2^n-bit table is replicated.
+__global__ void k_pad_small(const void *in, int kind, int n, uint32_t *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t pat = 0;
+    const int npts = 1 << n;
+    for (int x = 0; x < npts; x++) {
+        int bit;
+        if (kind == DQMC_IN_U8)
+            bit = ((const uint8_t *)in)[x] != 0;
+        else
+            bit = (int)((((const uint64_t *)in)[0] >> x) & 1ull);
+        pat |= (uint32_t)bit << x;
+    }
+    uint32_t w = 0;
+    for (int p = 0; p < 32; p++) w |= ((pat >> (p % npts)) & 1u) << p;
+    out[0] = w;
+}
+
+// splitmix64 finaliser (ttio.py:331-338)
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+// three-way generator: value of point x from the frozen
+// counter generator mix(seed + (x+1)*GAMMA) >> 11 (ttio.py:341-343, 365-374)
+__global__ void k_gen3(uint8_t *__restrict__ out, int64_t npts, uint64_t seed, uint64_t t_on, uint64_t t_any) {
+    const int64_t stride = gridDim.x * (int64_t)blockDim.x;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < npts; x += stride) {
+        const uint64_t u = mix64(seed + (uint64_t)(x + 1) * 0x9E3779B97F4A7C15ull) >> 11;
+        out[x] = u < t_on ? 1 : (u < t_any ? 2 : 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// contiguous C0 tile: 3^g blocks x 8 words in shared memory
+
+// MERGE of the C0 block axes on a tile whose 2^g binary blocks are loaded:
+// minimal-work order, each star block computed once (3^g - 2^g ANDs).
+__device__ void tile_merge_c0(uint32_t *sm, int g) {
+    for (int j = 0; j < g; j++) {
+        const int sj = (int)pow3l(j);
+        const int nhi = 1 << (g - 1 - j);
+        const int ntask = sj * nhi * 8;
+        for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+            const int w = t & 7, q = t >> 3;
+            const int lo = q % sj, hi = q / sj;
+            const int blk = lo + (int)bin_to_tern_rt(hi) * 3 * sj;
+            sm[(blk + 2 * sj) * 8 + w] = sm[blk * 8 + w] & sm[(blk + sj) * 8 + w];
+        }
+        __syncthreads();
+    }
+}
+
+// REDUCE along C0 axes [j0, j0+K) with register sub-cubes, lane = word.
+template <int K>
+__device__ void tile_reduce_axes(uint32_t *sm, int g, int j0) {
+    constexpr int N = P3<K>::v;
+    const int sj = (int)pow3l(j0);
+    const int span = sj * N;
+    const int nhi = (int)pow3l(g) / span;
+    const int ntask = sj * nhi * 8;
+    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+        const int w = t & 7, q = t >> 3;
+        const int lo = q % sj, hi = q / sj;
+        const int blk = lo + hi * span;
+        uint32_t v[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) v[i] = sm[(blk + i * sj) * 8 + w];
+        cube_reduce<K>(v);
+#pragma unroll
+        for (int i = 0; i < N; i++) sm[(blk + i * sj) * 8 + w] = v[i];
+    }
+    __syncthreads();
+}
+
+__device__ void tile_reduce_c0(uint32_t *sm, int g) {
+    int j = 0;
+    while (g - j >= 3) {
+        tile_reduce_axes<3>(sm, g, j);
+        j += 3;
+    }
+    if (g - j == 2) tile_reduce_axes<2>(sm, g, j);
+    if (g - j == 1) tile_reduce_axes<1>(sm, g, j);
+}
+
+struct FinalArgs {
+    int64_t *ranks;            // may be null (count only)
+    int64_t cap;               // capacity of ranks
+    int64_t rank_sub;          // subtracted from every rank (dummy-variable padding)
+    uint32_t ib_mask;          // in-block axes reduced in this pass
+    uint32_t *bitmap_out;      // write final bitmap here (null: do not)
+    unsigned long long *flags; // look-back descriptors, one per tile
+    int64_t *total;            // written by the last tile
+    int64_t ntiles;
+};
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+// In-block reduce, popcount, decoupled look-back and ordered compaction of one
+// tile (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order
+// is rank order, so the output needs no sort).
+__device__ void tile_finish(uint32_t *sm, int g, int64_t tile, int64_t blk0, const FinalArgs &fa) {
+    __shared__ int64_t s_warp_off[kTileThreads / 32];
+    __shared__ int64_t s_tile_off;
+    const int nb = (int)pow3l(g);
+    const int nwords = nb * 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+
+    // (1) in-block axes, thread per block
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        uint32_t v[8];
+        uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+        const uint4 x0 = p[0], x1 = p[1];
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        if (fa.ib_mask) inblock_reduce(v, fa.ib_mask);
+        const uint4 y0 = make_uint4(v[0], v[1], v[2], v[3]);
+        const uint4 y1 = make_uint4(v[4], v[5], v[6], v[7]);
+        p[0] = y0;
+        p[1] = y1;
+        if (fa.bitmap_out) {
+            uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+            q[0] = y0;
+            q[1] = y1;
+        }
+    }
+    __syncthreads();
+
+    // (2) warp-chunked counts: warp w owns words [w0, w1)
+    const int per = (nwords + nwarps - 1) / nwarps;
+    const int w0 = min(nwords, warp * per), w1 = min(nwords, w0 + per);
+    int cnt = 0;
+    for (int i = w0 + lane; i < w1; i += 32) cnt += __popc(sm[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_warp_off[warp] = cnt;
+    __syncthreads();
+
+    // (3) tile prefix: exclusive scan over warps + decoupled look-back
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int w = 0; w < nwarps; w++) {
+            const int64_t c = s_warp_off[w];
+            s_warp_off[w] = acc;
+            acc += c;
+        }
+        const int64_t agg = acc;
+        int64_t excl = 0;
+        volatile unsigned long long *flags = fa.flags;
+        if (tile == 0) {
+            __threadfence();
+            flags[0] = kFlagInc | (unsigned long long)agg;
+        } else {
+            flags[tile] = kFlagAgg | (unsigned long long)agg;
+            __threadfence();
+            int64_t p = tile - 1;
+            while (true) {
+                const unsigned long long f = flags[p];
+                const unsigned long long st = f & ~kValMask;
+                if (st == 0) continue;  // predecessor still running (it holds an earlier ticket)
+                excl += (int64_t)(f & kValMask);
+                if (st == kFlagInc) break;
+                p--;
+            }
+            __threadfence();
+            flags[tile] = kFlagInc | (unsigned long long)(excl + agg);
+        }
+        if (tile == fa.ntiles - 1) *fa.total = excl + agg;
+        s_tile_off = excl;
+    }
+    __syncthreads();
+    if (fa.ranks == nullptr) return;
+
+    // (4) ordered emission: lane = word, warp-inclusive scan of popcounts
+    int64_t off = s_tile_off + s_warp_off[warp];
+    for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        uint32_t w = (i < w1) ? sm[i] : 0u;
+        const int c = __popc(w);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int64_t pos = off + incl - c;
+        const int64_t rank0 = (blk0 + (i >> 3)) * 243 + (int64_t)(i & 7) * 32 - fa.rank_sub;
+        while (w) {
+            const int b = __ffs(w) - 1;
+            w &= w - 1;
+            if (pos < fa.cap) fa.ranks[pos] = rank0 + b;
+            pos++;
+        }
+        off += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// Load the binary blocks of a C0 tile from the truth table and merge it.
+// Tile index tb (binary over the top digits) selects 32-bit TT words
+// [tb << g, (tb+1) << g): point x = x_low5 + 32*(C0 bits) + 2^(5+g)*(top bits).
+__device__ void tile_build(uint32_t *sm, const uint32_t *__restrict__ tt32, int g, int64_t tb) {
+    const int nbin = 1 << g;
+    for (int e = threadIdx.x; e < nbin; e += blockDim.x) {
+        const uint32_t w = tt32[(tb << g) + e];
+        uint32_t v[8];
+        lm5(w, v);
+        const int pos = (int)bin_to_tern_rt((uint64_t)e);
+        uint4 *p = reinterpret_cast<uint4 *>(sm + pos * 8);
+        p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    }
+    __syncthreads();
+    tile_merge_c0(sm, g);
+}
+
+// pass A: top-binary tiles (2^T of them), merged over in-block + C0 axes
+__global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__restrict__ tt32,
+                                                           uint32_t *__restrict__ state, int g, int T) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int64_t ntiles = 1ll << T;
+    const int nb = (int)pow3l(g);
+    const int64_t p3g = pow3l(g);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int64_t base = 0, p = p3g;
+        for (int k = 0; k < T; k++, p *= 3)
+            if ((tile >> k) & 1) base += p;
+        tile_build(sm, tt32, g, tile);
+        uint4 *dst = reinterpret_cast<uint4 *>(state + base * 8);
+        const uint4 *src = reinterpret_cast<const uint4 *>(sm);
+        for (int t = threadIdx.x; t < nb * 2; t += blockDim.x) dst[t] = src[t];
+        __syncthreads();
+    }
+}
+
+// pass E: one CTA per C0 tile, tiles taken in rank order by ticket
+__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, int g,
+                                                           unsigned int *ticket, FinalArgs fa) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ int64_t s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int nb = (int)pow3l(g);
+    const int64_t blk0 = tile * nb;
+    const uint4 *src = reinterpret_cast<const uint4 *>(state + blk0 * 8);
+    uint4 *dst = reinterpret_cast<uint4 *>(sm);
+    for (int t = threadIdx.x; t < nb * 2; t += blockDim.x) dst[t] = __ldcs(src + t);
+    __syncthreads();
+    tile_reduce_c0(sm, g);
+    tile_finish(sm, g, tile, blk0, fa);
+}
+
+// n <= 12: the whole problem is one tile; one CTA does A and E.
+__global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restrict__ tt32, int g, FinalArgs fa) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    tile_build(sm, tt32, g, 0);
+    tile_reduce_c0(sm, g);
+    tile_finish(sm, g, 0, 0, fa);
+}
+
+// ---------------------------------------------------------------------------
+// strided group pass: R = R1 + R2 block axes at block stride Q = 3^a.
+// Tile = 3^R rows x 4 blocks (128 B); row rho = rho1 + 3^R1 * rho2.
+// Work item = (outer, column); lane = word within the 128-B row.
+
+template <int R1, int R2, int MODE>
+__global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restrict__ state, int64_t Q, int64_t ncol,
+                                                             int64_t nitems, uint32_t ib_mask) {
+    constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v, B1 = 1 << R1, B2 = 1 << R2;
+    constexpr int NR = N1 * N2;
+    extern __shared__ __align__(16) uint32_t sm[];  // NR rows x 32 words
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int64_t Qw = Q * 8;  // row stride in words
+
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int64_t col = item % ncol;
+        const int64_t outer = item / ncol;
+        const int64_t ob = (MODE == MERGE_ONLY) ? bin_to_tern_rt((uint64_t)outer) : outer;
+        const int64_t c0 = col * kRowBlocks;
+        const int valid = (int)min((int64_t)kRowBlocks, Q - c0) * 8;
+        const bool act = lane < valid;
+        uint32_t *g0 = state + (ob * NR * Q + c0) * 8 + lane;  // word of row 0
+        // in-block round needed?
+        const bool ib = (MODE != MERGE_ONLY) && ib_mask != 0;
+
+        if (MODE == MERGE_ONLY || MODE == MERGE_REDUCE) {
+            // round 1: for each binary rho2, merge the R1 axes
+            for (int t2 = warp; t2 < B2; t2 += nwarps) {
+                const int r2 = (int)bin_to_tern_rt((uint64_t)t2);
+                uint32_t v[N1];
+#pragma unroll
+                for (int i = 0; i < N1; i++) v[i] = 0;
+#pragma unroll
+                for (int b = 0; b < B1; b++) {
+                    const int r1 = bin_to_tern(b);
+                    v[r1] = act ? g0[(int64_t)(r1 + N1 * r2) * Qw] : 0u;
+                }
+                cube_merge<R1>(v);
+                if (MODE == MERGE_REDUCE && R2 == 0) {
+                    cube_reduce<R1>(v);
+#pragma unroll
+                    for (int i = 0; i < N1; i++) {
+                        if (ib)
+                            sm[(i + N1 * r2) * 32 + lane] = v[i];
+                        else if (act)
+                            g0[(int64_t)(i + N1 * r2) * Qw] = v[i];
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < N1; i++) {
+                        if (MODE == MERGE_ONLY && has_star(i, R1) && act) g0[(int64_t)(i + N1 * r2) * Qw] = v[i];
+                        if (R2 > 0) sm[(i + N1 * r2) * 32 + lane] = v[i];
+                    }
+                }
+            }
+            __syncthreads();
+            if (R2 > 0) {
+                // round 2: for each rho1, merge the R2 axes (+ reduce them)
+                for (int t1 = warp; t1 < N1; t1 += nwarps) {
+                    uint32_t v[N2];
+#pragma unroll
+                    for (int i = 0; i < N2; i++) v[i] = 0;
+#pragma unroll
+                    for (int b = 0; b < B2; b++) {
+                        const int r2 = bin_to_tern(b);
+                        v[r2] = sm[(t1 + N1 * r2) * 32 + lane];
+                    }
+                    cube_merge<R2>(v);
+                    if (MODE == MERGE_ONLY) {
+#pragma unroll
+                        for (int i = 0; i < N2; i++)
+                            if (has_star(i, R2) && act) g0[(int64_t)(t1 + N1 * i) * Qw] = v[i];
+                    } else {
+                        cube_reduce<R2>(v);
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < N2; i++) sm[(t1 + N1 * i) * 32 + lane] = v[i];
+                    }
+                }
+                __syncthreads();
+                if (MODE == MERGE_REDUCE) {
+                    // round 3: reduce the R1 axes
+                    for (int t2 = warp; t2 < N2; t2 += nwarps) {
+                        uint32_t v[N1];
+#pragma unroll
+                        for (int i = 0; i < N1; i++) v[i] = sm[(i + N1 * t2) * 32 + lane];
+                        cube_reduce<R1>(v);
+#pragma unroll
+                        for (int i = 0; i < N1; i++) {
+                            if (ib)
+                                sm[(i + N1 * t2) * 32 + lane] = v[i];
+                            else if (act)
+                                g0[(int64_t)(i + N1 * t2) * Qw] = v[i];
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+        } else {  // REDUCE_ONLY
+            // round 1: reduce the R1 axes, rows straight from HBM
+            for (int t2 = warp; t2 < N2; t2 += nwarps) {
+                uint32_t v[N1];
+#pragma unroll
+                for (int i = 0; i < N1; i++) v[i] = act ? __ldcs(g0 + (int64_t)(i + N1 * t2) * Qw) : 0u;
+                cube_reduce<R1>(v);
+#pragma unroll
+                for (int i = 0; i < N1; i++) {
+                    if (R2 > 0 || ib)
+                        sm[(i + N1 * t2) * 32 + lane] = v[i];
+                    else if (act)
+                        g0[(int64_t)(i + N1 * t2) * Qw] = v[i];
+                }
+            }
+            __syncthreads();
+            if (R2 > 0) {
+                for (int t1 = warp; t1 < N1; t1 += nwarps) {
+                    uint32_t v[N2];
+#pragma unroll
+                    for (int i = 0; i < N2; i++) v[i] = sm[(t1 + N1 * i) * 32 + lane];
+                    cube_reduce<R2>(v);
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < N2; i++) {
+                        if (ib)
+                            sm[(t1 + N1 * i) * 32 + lane] = v[i];
+                        else if (act)
+                            g0[(int64_t)(t1 + N1 * i) * Qw] = v[i];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+
+        if (ib) {
+            // in-block axes: thread per (row, block); 32-B stores
+            const int nblk_valid = valid / 8;
+            for (int t = threadIdx.x; t < NR * kRowBlocks; t += blockDim.x) {
+                const int row = t >> 2, b = t & 3;
+                if (b >= nblk_valid) continue;
+                uint4 *p = reinterpret_cast<uint4 *>(sm + row * 32 + b * 8);
+                const uint4 x0 = p[0], x1 = p[1];
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, ib_mask);
+                uint4 *q = reinterpret_cast<uint4 *>(state + (ob * NR * Q + (int64_t)row * Q + c0 + b) * 8);
+                q[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                q[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct Plan {
+    int n = 0, ne = 0;  // requested / effective (>= 5) variable count
+    int H = 0, g = 0, T = 0, m = 0;
+    int r[8] = {0}, a[8] = {0};
+    uint32_t ib_C = 0, ib_E = 0, ib_D[8] = {0};
+    int64_t rank_sub = 0;
+    int64_t nblocks = 0;
+};
+
+Plan make_plan(int n) {
+    Plan p;
+    p.n = n;
+    p.ne = n < 5 ? 5 : n;
+    p.rank_sub = n < 5 ? (243 - pow3l(n)) : 0;
+    p.H = p.ne - 5;
+    p.g = std::min(p.H, kC0Max);
+    p.T = p.H - p.g;
+    p.nblocks = pow3l(p.H);
+    if (p.T > 0) {
+        p.m = (p.T + kGroupMax - 1) / kGroupMax;
+        int a = p.g;
+        for (int k = 0; k < p.m; k++) {
+            const int rk = p.T / p.m + (k < p.T % p.m ? 1 : 0);
+            p.r[k] = rk;
+            p.a[k] = a;
+            a += rk;
+        }
+    }
+    // distribute the five in-block REDUCE axes over the passes that hold whole
+    // blocks (pass C: 1, each pass D: 2, pass E: 1; leftovers alternate C/E)
+    if (p.T == 0) {
+        p.ib_E = 31u;
+    } else {
+        int axis = 0;
+        auto take = [&](uint32_t &mask, int cnt) {
+            for (int c = 0; c < cnt && axis < 5; c++) mask |= 1u << axis++;
+        };
+        take(p.ib_C, 1);
+        for (int k = p.m - 2; k >= 0; k--) take(p.ib_D[k], 2);
+        take(p.ib_E, 1);
+        bool toC = false;
+        while (axis < 5) {
+            take(toC ? p.ib_C : p.ib_E, 1);
+            toC = !toC;
+        }
+    }
+    return p;
+}
+
+thread_local std::string g_err;
+std::mutex g_mu;
+
+int set_err(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                         \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) return set_err(DQMC_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct PinnedBuf {
+    int64_t *ptr = nullptr;
+    size_t cap = 0;  // entries
+};
+
+struct Engine {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    uint32_t *state = nullptr;
+    size_t state_cap = 0;  // bytes
+    unsigned long long *flags = nullptr;
+    size_t flags_cap = 0;  // entries
+    unsigned int *ticket = nullptr;
+    int64_t *total = nullptr;
+    uint32_t *tt_tmp = nullptr;
+    size_t tt_tmp_cap = 0;  // bytes
+    void *in_tmp = nullptr;
+    size_t in_tmp_cap = 0;
+    int64_t *ranks = nullptr;
+    size_t ranks_cap = 0;  // entries
+    std::vector<PinnedBuf> free_pinned;
+    // timings of the last DQMC_FLAG_TIMING call
+    std::vector<std::string> pass_names;
+    std::vector<float> pass_ms;
+    std::vector<uint64_t> pass_bytes;
+    int state_n = -1;  // n whose final bitmap is held in `state` (KEEP_BITMAP)
+    bool attrs_set = false;
+};
+
+Engine g_eng;
+
+int ensure_device() {
+    if (g_eng.device >= 0) return DQMC_OK;
+    int cnt = 0;
+    cudaError_t e = cudaGetDeviceCount(&cnt);
+    if (e != cudaSuccess || cnt == 0)
+        return set_err(DQMC_ERR_NODEVICE, "no CUDA device visible: libdqmc has no CPU fallback");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaSetDevice(dev));
+    g_eng.device = dev;
+    CK(cudaStreamCreateWithFlags(&g_eng.stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&g_eng.ticket, 256));
+    CK(cudaMalloc(&g_eng.total, 256));
+    return DQMC_OK;
+}
+
+template <typename T>
+int grow(T *&ptr, size_t &cap, size_t need, size_t elem) {
+    if (need <= cap && ptr) return DQMC_OK;
+    if (ptr) {
+        cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    cudaError_t e = cudaMalloc((void **)&ptr, need * elem);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        ptr = nullptr;
+        char buf[256];
+        snprintf(buf, sizeof buf, "device allocation of %llu bytes failed: %s", (unsigned long long)(need * elem),
+                 cudaGetErrorString(e));
+        return set_err(DQMC_ERR_RESOURCE, buf);
+    }
+    cap = need;
+    return DQMC_OK;
+}
+
+template <int R1, int R2, int MODE>
+int set_strided_attr() {
+    constexpr int smem = P3<R1>::v * P3<R2>::v * 32 * 4;
+    CK(cudaFuncSetAttribute(k_strided<R1, R2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return DQMC_OK;
+}
+
+template <int MODE>
+int set_mode_attrs() {
+    int rc;
+    if ((rc = set_strided_attr<1, 0, MODE>())) return rc;
+    if ((rc = set_strided_attr<2, 0, MODE>())) return rc;
+    if ((rc = set_strided_attr<3, 0, MODE>())) return rc;
+    if ((rc = set_strided_attr<2, 2, MODE>())) return rc;
+    if ((rc = set_strided_attr<3, 2, MODE>())) return rc;
+    if ((rc = set_strided_attr<3, 3, MODE>())) return rc;
+    return DQMC_OK;
+}
+
+int ensure_attrs() {
+    if (g_eng.attrs_set) return DQMC_OK;
+    const int tile_smem = (int)pow3l(kC0Max) * 32;
+    CK(cudaFuncSetAttribute(k_c0_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    CK(cudaFuncSetAttribute(k_c0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    int rc;
+    if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;
+    if ((rc = set_mode_attrs<MERGE_REDUCE>())) return rc;
+    if ((rc = set_mode_attrs<REDUCE_ONLY>())) return rc;
+    g_eng.attrs_set = true;
+    return DQMC_OK;
+}
+
+struct Timer {
+    bool on;
+    cudaStream_t s;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::string> names;
+    std::vector<uint64_t> bytes;
+    void mark(const char *name, uint64_t b) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+        names.push_back(name);
+        bytes.push_back(b);
+    }
+    void begin() {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+    }
+    void finish() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back());
+        g_eng.pass_names.clear();
+        g_eng.pass_ms.clear();
+        g_eng.pass_bytes.clear();
+        for (size_t i = 1; i < ev.size(); i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            g_eng.pass_ms.push_back(ms);
+            g_eng.pass_names.push_back(names[i - 1]);
+            g_eng.pass_bytes.push_back(bytes[i - 1]);
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        ev.clear();
+    }
+};
+
+template <int MODE>
+void launch_strided_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nitems, uint32_t ib,
+                         cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(nitems, 148ll * 16);
+#define LS(R1, R2)                                                                             \
+    k_strided<R1, R2, MODE><<<grid, kStridedThreads, P3<R1>::v * P3<R2>::v * 32 * 4, s>>>(state, Q, ncol, \
+                                                                                        nitems, ib)
+    switch (r) {
+        case 1: LS(1, 0); break;
+        case 2: LS(2, 0); break;
+        case 3: LS(3, 0); break;
+        case 4: LS(2, 2); break;
+        case 5: LS(3, 2); break;
+        default: LS(3, 3); break;
+    }
+#undef LS
+}
+
+uint64_t state_bytes_ref(int n, int h) {
+    // dense.py:56-63
+    uint64_t used = (uint64_t)pow3l(h), b = 1;
+    while (b < used) b <<= 1;
+    if (b < 64) b = 64;
+    return (uint64_t)pow3l(n - h) * b / 8;
+}
+
+uint64_t engine_device_bytes(const Plan &p, bool keep) {
+    if (p.T == 0 && !keep) return 0;
+    return (uint64_t)p.nblocks * 32 + (uint64_t)pow3l(p.T) * 8;
+}
+
+// Run the whole plan on a device-resident 32-bit truth table.
+int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, int64_t *count, uint32_t flags,
+             cudaStream_t s) {
+    Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
+    const bool keep = (flags & DQMC_FLAG_KEEP_BITMAP) != 0;
+    int rc;
+    const uint64_t S = (uint64_t)p.nblocks * 32;
+    if (p.T > 0 || keep) {
+        if ((rc = grow(g_eng.state, g_eng.state_cap, S, 1))) return rc;
+    }
+    if ((rc = grow(g_eng.flags, g_eng.flags_cap, (size_t)std::max<int64_t>(1, pow3l(p.T)), 8))) return rc;
+    FinalArgs fa;
+    fa.ranks = (flags & DQMC_FLAG_COUNT_ONLY) ? nullptr : ranks;
+    fa.cap = fa.ranks ? cap : 0;
+    fa.rank_sub = p.rank_sub;
+    fa.flags = g_eng.flags;
+    fa.total = g_eng.total;
+    fa.bitmap_out = keep ? g_eng.state : nullptr;
+    const int tile_smem = (int)pow3l(p.g) * 32;
+    tm.begin();
+    if (p.T == 0) {
+        fa.ib_mask = p.ib_E;
+        fa.ntiles = 1;
+        k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
+        CK(cudaGetLastError());
+        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (keep ? S : 0));
+    } else {
+        // pass A
+        const int64_t ntA = 1ll << p.T;
+        const int gridA = (int)std::min<int64_t>(ntA, 148ll * 8);
+        k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, g_eng.state, p.g, p.T);
+        CK(cudaGetLastError());
+        tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
+        // fraction helper: (2/3)^k of S
+        auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
+        // passes B: merge-only groups 0..m-2 (outer digits of higher groups binary)
+        for (int k = 0; k + 1 < p.m; k++) {
+            const int64_t Q = pow3l(p.a[k]);
+            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+            int above = 0;
+            for (int j = k + 1; j < p.m; j++) above += p.r[j];
+            const int64_t nitems = ncol << above;
+            launch_strided_mode<MERGE_ONLY>(p.r[k], g_eng.state, Q, ncol, nitems, 0, s);
+            CK(cudaGetLastError());
+            tm.mark("k_strided<MERGE_ONLY>", (uint64_t)(frac(above + p.r[k]) + (frac(above) - frac(above + p.r[k]))));
+        }
+        // pass C: last group, merge + reduce
+        {
+            const int k = p.m - 1;
+            const int64_t Q = pow3l(p.a[k]);
+            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+            launch_strided_mode<MERGE_REDUCE>(p.r[k], g_eng.state, Q, ncol, ncol, p.ib_C, s);
+            CK(cudaGetLastError());
+            tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(frac(p.r[k]) + S));
+        }
+        // passes D: reduce the other groups
+        for (int k = p.m - 2; k >= 0; k--) {
+            const int64_t Q = pow3l(p.a[k]);
+            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+            int above = 0;
+            for (int j = k + 1; j < p.m; j++) above += p.r[j];
+            const int64_t nitems = ncol * pow3l(above);
+            launch_strided_mode<REDUCE_ONLY>(p.r[k], g_eng.state, Q, ncol, nitems, p.ib_D[k], s);
+            CK(cudaGetLastError());
+            tm.mark("k_strided<REDUCE>", 2 * S);
+        }
+        // pass E
+        const int64_t ntiles = pow3l(p.T);
+        CK(cudaMemsetAsync(g_eng.ticket, 0, sizeof(unsigned int), s));
+        CK(cudaMemsetAsync(g_eng.flags, 0, (size_t)ntiles * 8, s));
+        fa.ib_mask = p.ib_E;
+        fa.ntiles = ntiles;
+        k_c0_final<<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, p.g, g_eng.ticket, fa);
+        CK(cudaGetLastError());
+        tm.mark("k_c0_final", S + (keep ? S : 0));
+    }
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tm.finish();
+    *count = total;
+    g_eng.state_n = keep ? p.n : -1;
+    return DQMC_OK;
+}
+
+// total device pass (input conversion + plan) with growable rank buffer
+int primes_device_impl(const void *in, int kind, int n, int64_t *ranks, int64_t cap, int64_t *count,
+                       uint32_t flags, cudaStream_t s) {
+    const Plan p = make_plan(n);
+    const uint32_t *tt32 = nullptr;
+    int rc;
+    if (n < 5) {
+        if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, 256, 1))) return rc;
+        k_pad_small<<<1, 32, 0, s>>>(in, kind, n, g_eng.tt_tmp);
+        CK(cudaGetLastError());
+        tt32 = g_eng.tt_tmp;
+    } else if (kind == DQMC_IN_U8) {
+        const int64_t nw = 1ll << (n - 5);
+        if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, (size_t)nw * 4, 1))) return rc;
+        const int grid = (int)std::min<int64_t>((nw * 32 + 255) / 256, 148ll * 32);
+        k_u8_to_words<<<grid, 256, 0, s>>>((const uint8_t *)in, g_eng.tt_tmp, nw);
+        CK(cudaGetLastError());
+        tt32 = g_eng.tt_tmp;
+    } else {
+        tt32 = (const uint32_t *)in;  // LE uint64 words viewed as uint32 words
+    }
+    return run_plan(p, tt32, ranks, cap, count, flags, s);
+}
+
+int validate(int n, int h) {
+    if (n < 1 || n > 31) return set_err(DQMC_ERR_INVALID, "variable count must be in 1..31, got " + std::to_string(n));
+    if (h != 0 && (h < 1 || h > n))
+        return set_err(DQMC_ERR_INVALID,
+                       "split must be in 1.." + std::to_string(n) + ", got " + std::to_string(h));
+    return DQMC_OK;
+}
+
+// dense.py:358-364: refuse before allocating, message names the bytes
+int check_cap(int n, int h, uint64_t mem_cap, uint64_t device_need) {
+    const int hh = h == 0 ? std::min(n, 5) : h;
+    const uint64_t need = state_bytes_ref(n, hh);
+    uint64_t cap = mem_cap;
+    if (cap == 0) {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        cap = (uint64_t)((double)(fr + g_eng.state_cap + g_eng.ranks_cap * 8) * 0.75);
+    }
+    uint64_t bb = (uint64_t)state_bytes_ref(hh, hh) * 8;
+    char buf[512];
+    if (need > cap) {
+        snprintf(buf, sizeof buf,
+                 "dense state needs %llu bytes (%lld blocks of %llu bits), exceeding the cap of %llu bytes",
+                 (unsigned long long)need, (long long)pow3l(n - hh), (unsigned long long)bb,
+                 (unsigned long long)cap);
+        return set_err(DQMC_ERR_RESOURCE, buf);
+    }
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const uint64_t have = (uint64_t)fr + g_eng.state_cap;
+    if (device_need > have) {
+        snprintf(buf, sizeof buf, "device state needs %llu bytes, only %llu bytes of device memory are free",
+                 (unsigned long long)device_need, (unsigned long long)have);
+        return set_err(DQMC_ERR_RESOURCE, buf);
+    }
+    return DQMC_OK;
+}
+
+int alloc_pinned(size_t entries, PinnedBuf &out) {
+    // reuse the smallest cached buffer that fits
+    int best = -1;
+    for (size_t i = 0; i < g_eng.free_pinned.size(); i++)
+        if (g_eng.free_pinned[i].cap >= entries && (best < 0 || g_eng.free_pinned[i].cap < g_eng.free_pinned[best].cap))
+            best = (int)i;
+    if (best >= 0) {
+        out = g_eng.free_pinned[best];
+        g_eng.free_pinned.erase(g_eng.free_pinned.begin() + best);
+        return DQMC_OK;
+    }
+    size_t want = std::max<size_t>(entries, 1024);
+    int64_t *p = nullptr;
+    cudaError_t e = cudaHostAlloc((void **)&p, want * 8, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        char buf[160];
+        snprintf(buf, sizeof buf, "pinned host allocation of %llu bytes failed", (unsigned long long)(want * 8));
+        return set_err(DQMC_ERR_RESOURCE, buf);
+    }
+    out.ptr = p;
+    out.cap = want;
+    return DQMC_OK;
+}
+
+int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_cap, uint32_t flags,
+                     dqmc_result_t *out) {
+    if (!out) return set_err(DQMC_ERR_INVALID, "null result pointer");
+    out->count = 0;
+    out->ranks = nullptr;
+    out->_owner = nullptr;
+    int rc;
+    if ((rc = validate(n, h))) return rc;
+    if (!host_in) return set_err(DQMC_ERR_INVALID, "null input pointer");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    const Plan p = make_plan(n);
+    if ((rc = check_cap(n, h, mem_cap, engine_device_bytes(p, flags & DQMC_FLAG_KEEP_BITMAP)))) return rc;
+    cudaStream_t s = g_eng.stream;
+    // H2D of the input (pageable source; small relative to the state)
+    const size_t in_bytes = kind == DQMC_IN_U8 ? ((size_t)1 << n) : (size_t)std::max<int64_t>(1, (1ll << n) / 64) * 8;
+    if ((rc = grow(g_eng.in_tmp, g_eng.in_tmp_cap, std::max<size_t>(in_bytes, 8), 1))) return rc;
+    CK(cudaMemcpyAsync(g_eng.in_tmp, host_in, in_bytes, cudaMemcpyHostToDevice, s));
+    const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0;
+    if (!count_only && g_eng.ranks_cap == 0) {
+        if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)1 << 20, 8))) return rc;
+    }
+    int64_t count = 0;
+    if ((rc = primes_device_impl(g_eng.in_tmp, kind, n, count_only ? nullptr : g_eng.ranks, (int64_t)g_eng.ranks_cap,
+                                 &count, flags, s)))
+        return rc;
+    if (!count_only && (size_t)count > g_eng.ranks_cap) {
+        // grow the output and run again (only the count was exact)
+        if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)((double)count * 1.05) + 1024, 8))) return rc;
+        if ((rc = primes_device_impl(g_eng.in_tmp, kind, n, g_eng.ranks, (int64_t)g_eng.ranks_cap, &count, flags, s)))
+            return rc;
+    }
+    out->count = count;
+    if (!count_only && count > 0) {
+        PinnedBuf pb;
+        if ((rc = alloc_pinned((size_t)count, pb))) return rc;
+        CK(cudaMemcpyAsync(pb.ptr, g_eng.ranks, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        PinnedBuf *owner = new PinnedBuf(pb);
+        out->ranks = pb.ptr;
+        out->_owner = owner;
+    }
+    return DQMC_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int dqmc_abi_version(void) { return DQMC_ABI_VERSION; }
+
+const char *dqmc_last_error(void) { return g_err.c_str(); }
+
+int dqmc_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+int dqmc_set_device(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_eng.device == device) return DQMC_OK;
+    if (g_eng.device >= 0) return set_err(DQMC_ERR_INVALID, "device already selected; call dqmc_release first");
+    CK(cudaSetDevice(device));
+    return DQMC_OK;
+}
+
+uint64_t dqmc_block_bits(int h) { return state_bytes_ref(h, h) * 8; }
+
+uint64_t dqmc_state_bytes(int n, int h) { return state_bytes_ref(n, h); }
+
+uint64_t dqmc_device_bytes(int n) {
+    if (n < 1 || n > 31) return 0;
+    return engine_device_bytes(make_plan(n), false);
+}
+
+int dqmc_primes_tt(const uint64_t *tt_words, int n, int h, uint64_t mem_cap, uint32_t flags, dqmc_result_t *out) {
+    return primes_host_impl(tt_words, DQMC_IN_WORDS, n, h, mem_cap, flags, out);
+}
+
+int dqmc_primes_u8(const uint8_t *values, int n, int h, uint64_t mem_cap, uint32_t flags, dqmc_result_t *out) {
+    return primes_host_impl(values, DQMC_IN_U8, n, h, mem_cap, flags, out);
+}
+
+void dqmc_free_result(dqmc_result_t *res) {
+    if (!res) return;
+    if (res->_owner) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        PinnedBuf *pb = (PinnedBuf *)res->_owner;
+        g_eng.free_pinned.push_back(*pb);
+        // keep at most two cached pinned buffers
+        while (g_eng.free_pinned.size() > 2) {
+            auto it = std::min_element(g_eng.free_pinned.begin(), g_eng.free_pinned.end(),
+                                       [](const PinnedBuf &a, const PinnedBuf &b) { return a.cap < b.cap; });
+            cudaFreeHost(it->ptr);
+            g_eng.free_pinned.erase(it);
+        }
+        delete pb;
+    }
+    res->_owner = nullptr;
+    res->ranks = nullptr;
+    res->count = 0;
+}
+
+int dqmc_primes_device(const void *input_dev, int in_kind, int n, int64_t *ranks_dev, int64_t ranks_cap,
+                       int64_t *count_out, uint32_t flags, void *stream) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (!input_dev || !count_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    if (in_kind != DQMC_IN_WORDS && in_kind != DQMC_IN_U8) return set_err(DQMC_ERR_INVALID, "bad input kind");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    const Plan p = make_plan(n);
+    if ((rc = check_cap(n, 0, 0, engine_device_bytes(p, flags & DQMC_FLAG_KEEP_BITMAP)))) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    if (!ranks_dev) flags |= DQMC_FLAG_COUNT_ONLY;
+    return primes_device_impl(input_dev, in_kind, n, ranks_dev, ranks_cap, count_out, flags, s);
+}
+
+int dqmc_last_timings(const char **names, float *ms, int max) {
+    const int k = (int)g_eng.pass_ms.size();
+    for (int i = 0; i < k && i < max; i++) {
+        if (names) names[i] = g_eng.pass_names[i].c_str();
+        if (ms) ms[i] = g_eng.pass_ms[i];
+    }
+    return k;
+}
+
+int dqmc_last_pass_bytes(uint64_t *bytes, int max) {
+    const int k = (int)g_eng.pass_bytes.size();
+    for (int i = 0; i < k && i < max; i++) bytes[i] = g_eng.pass_bytes[i];
+    return k;
+}
+
+int dqmc_state_device(void **ptr, uint64_t *bytes) {
+    if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
+    const Plan p = make_plan(g_eng.state_n);
+    if (ptr) *ptr = g_eng.state;
+    if (bytes) *bytes = (uint64_t)p.nblocks * 32;
+    return DQMC_OK;
+}
+
+int dqmc_state_download(void *host, uint64_t bytes) {
+    if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
+    const Plan p = make_plan(g_eng.state_n);
+    const uint64_t need = (uint64_t)p.nblocks * 32;
+    if (bytes < need) return set_err(DQMC_ERR_INVALID, "host buffer too small");
+    CK(cudaMemcpy(host, g_eng.state, need, cudaMemcpyDeviceToHost));
+    return DQMC_OK;
+}
+
+int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint64_t seed, void *stream) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    // int(p * 2^53) as Python computes it (float64 product, truncation)
+    const uint64_t t_on = (uint64_t)(p_on * 9007199254740992.0);
+    const uint64_t t_any = (uint64_t)((p_on + p_dc) * 9007199254740992.0);
+    const int64_t npts = 1ll << n;
+    const int grid = (int)std::min<int64_t>((npts + 255) / 256, 148ll * 64);
+    k_gen3<<<grid, 256, 0, s>>>(values_dev, npts, seed, t_on, t_any);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return DQMC_OK;
+}
+
+int dqmc_plan(int n, int64_t *out, int max) {
+    if (n < 1 || n > 31 || !out) return 0;
+    const Plan p = make_plan(n);
+    int64_t v[32];
+    int k = 0;
+    v[k++] = p.ne;
+    v[k++] = p.H;
+    v[k++] = p.g;
+    v[k++] = p.T;
+    v[k++] = p.m;
+    for (int i = 0; i < 8; i++) v[k++] = p.r[i];
+    for (int i = 0; i < 8; i++) v[k++] = p.a[i];
+    v[k++] = p.ib_C;
+    v[k++] = p.ib_E;
+    for (int i = 0; i < 8; i++) v[k++] = p.ib_D[i];
+    v[k++] = p.rank_sub;
+    const int w = std::min(k, max);
+    for (int i = 0; i < w; i++) out[i] = v[i];
+    return w;
+}
+
+void dqmc_release(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_eng.device < 0) return;
+    cudaFree(g_eng.state);
+    cudaFree(g_eng.flags);
+    cudaFree(g_eng.ticket);
+    cudaFree(g_eng.total);
+    cudaFree(g_eng.tt_tmp);
+    cudaFree(g_eng.in_tmp);
+    cudaFree(g_eng.ranks);
+    for (auto &b : g_eng.free_pinned) cudaFreeHost(b.ptr);
+    if (g_eng.stream) cudaStreamDestroy(g_eng.stream);
+    g_eng = Engine();
+}
+
+}  // extern "C"

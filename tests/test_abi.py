@@ -1,0 +1,114 @@
+"""C-ABI boundary checks that run without a GPU.
+
+* libdqmc.so loads and exports every function include/dqmc.h declares;
+* size helpers agree with the reference formulas (dense.py:56-63);
+* argument validation and resource errors behave as the reference's
+  (ValueError / ResourceLimitError naming the bytes) before any GPU use;
+* with no CUDA device a compute call fails loudly — there is no CPU fallback.
+"""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(REPO, "include", "dqmc.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dqmc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(pkg):
+    from paper_2302_10083_b200 import _lib
+
+    L = _lib.load()
+    declared = header_functions()
+    assert declared, "no functions parsed from include/dqmc.h"
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(_lib.EXPORTS) == declared
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared:
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_abi_version_and_sizes(pkg):
+    from paper_2302_10083_b200 import _lib
+
+    L = _lib.load()
+    assert L.dqmc_abi_version() == 1
+    for h in range(1, 10):
+        assert L.dqmc_block_bits(h) == pkg.block_bits_for(h)
+    for n in range(1, 28):
+        for h in range(1, min(n, 8) + 1):
+            assert L.dqmc_state_bytes(n, h) == 3 ** (n - h) * pkg.block_bits_for(h) // 8
+    # tests/test_dense.py:72-84 pins
+    assert pkg.block_bits_for(1) == 64 and pkg.block_bits_for(3) == 64
+    assert pkg.block_bits_for(4) == 128 and pkg.block_bits_for(5) == 256
+    assert pkg.state_bytes(3, 1) == 72 and pkg.state_bytes(20, 5) == 3**15 * 32
+
+
+def test_plan_covers_every_axis(pkg):
+    from paper_2302_10083_b200 import _lib
+
+    for n in range(1, 28):
+        p = _lib.plan(n)
+        assert p["ne"] == max(n, 5) and p["H"] == p["ne"] - 5
+        assert p["g"] + p["T"] == p["H"] and p["g"] <= 7
+        assert sum(p["r"]) == p["T"] and all(0 < r <= 6 for r in p["r"][: p["m"]])
+        a = p["g"]
+        for k in range(p["m"]):
+            assert p["a"][k] == a
+            a += p["r"][k]
+        masks = [p["ib_C"], p["ib_E"]] + p["ib_D"][: max(0, p["m"] - 1)]
+        acc = 0
+        for m in masks:
+            assert acc & m == 0  # each in-block axis reduced exactly once
+            acc |= m
+        assert acc == 31
+        assert p["rank_sub"] == (243 - 3**n if n < 5 else 0)
+
+
+def test_validation_before_gpu(pkg):
+    tt = pkg.TruthTable.empty(3)
+    with pytest.raises(ValueError):
+        pkg.dense_prime_ranks(tt, h=0)
+    with pytest.raises(ValueError):
+        pkg.dense_prime_ranks(tt, h=4)
+    tt12 = pkg.TruthTable.empty(12)
+    need = pkg.state_bytes(12, 5)
+    with pytest.raises(pkg.ResourceLimitError) as exc:
+        pkg.dense_prime_ranks(tt12, h=5, mem_cap=0)
+    assert str(need) in str(exc.value) and "bytes" in str(exc.value)
+    with pytest.raises(ValueError):
+        pkg.TruthTable(3, np.zeros(2, dtype=np.uint64))
+    with pytest.raises(ValueError):
+        pkg.run_engine("fastest", tt)
+
+
+def test_no_device_fails_loudly(pkg):
+    from paper_2302_10083_b200 import _lib
+
+    if _lib.load().dqmc_device_count() > 0:
+        pytest.skip("a CUDA device is visible")
+    with pytest.raises(RuntimeError, match="CUDA device required"):
+        pkg.dense_prime_ranks(pkg.TruthTable.full(4))
+    res = _lib.DqmcResult()
+    w = np.zeros(16, dtype=np.uint64)
+    rc = _lib.load().dqmc_primes_tt(w.ctypes.data, 10, 0, 0, 0, ctypes.byref(res))
+    assert rc == _lib.DQMC_ERR_NODEVICE
+
+
+def test_ternary_helpers(pkg):
+    assert pkg.rank("1*0**") == 223  # SPEC.md rank example
+    assert pkg.unrank(223, 5) == "1*0**"
+    assert pkg.index_to_rank(np.array([7]), 3).tolist() == [13]
+    assert pkg.unrank_many(np.array([14, 16, 22]), 3) == ["*11", "1*1", "11*"]
+    assert pkg.ranks_to_text(np.array([14]), 3, wildcard="-") == "-11\n"
+    assert pkg.rank_weights(np.array([26, 0]), 3).tolist() == [3, 0]

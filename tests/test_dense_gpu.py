@@ -1,0 +1,177 @@
+"""Parity of the B200 engine (libdqmc.so through the C ABI) with the oracle.
+
+Bar: bit-exact int64 rank arrays. Small sizes are compared against the
+committed reference goldens and the C oracle; n=24 (BASELINE config 4) is
+pinned by the reference's recorded count and rank hash, plus sortedness and a
+sampled independent implicant/maximality check.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rsha(r):
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(r, dtype="<i8")).tobytes()).hexdigest()
+
+
+def tt_of(pkg, gen_mod, n, d, s):
+    return pkg.TruthTable(n, gen_mod.random_words(n, d, s))
+
+
+class TestKnownAnswers:
+    def test_maj3_and_frozen(self, pkg, golden):
+        maj3 = pkg.TruthTable.from_indices(3, [3, 5, 6, 7])
+        assert pkg.dense_prime_ranks(maj3).tolist() == [14, 16, 22]
+        assert pkg.find_primes_dense(maj3) == {"*11", "1*1", "11*"}
+        assert pkg.dense_prime_ranks(pkg.TruthTable.from_indices(5, [12, 14])).tolist() == [42]
+        assert pkg.find_primes_dense(pkg.TruthTable.from_indices(5, [0b01100, 0b01110])) == {"0*110"}
+        assert pkg.find_primes_dense(pkg.TruthTable.from_indices(6, [0b101001])) == {"100101"}
+        bits = golden["known"]["cli_order_bits"]
+        tt = pkg.TruthTable.from_bools(4, np.array([c == "1" for c in bits]))
+        assert pkg.dense_prime_ranks(tt).tolist() == golden["known"]["cli_order_ranks"]
+
+    def test_constant_and_empty(self, pkg):
+        for n in range(1, 16):
+            r = pkg.dense_prime_ranks(pkg.TruthTable.full(n))
+            assert r.tolist() == [3**n - 1], n
+            e = pkg.dense_prime_ranks(pkg.TruthTable.empty(n))
+            assert e.dtype == np.int64 and e.shape == (0,), n
+
+    def test_extract_equals_support_for_isolated_points(self, pkg):
+        # points pairwise at Hamming distance >= 2 are their own primes
+        tt = pkg.TruthTable.from_indices(4, [0, 5, 9, 14])
+        assert pkg.find_primes_dense(tt) == {"0000", "1010", "1001", "0111"}
+
+
+class TestSweeps:
+    def test_acceptance_sweep_c1(self, pkg, golden, gen_mod):
+        for n, d, s, cnt, h16 in golden["sweep_c1"]:
+            r = pkg.dense_prime_ranks(tt_of(pkg, gen_mod, n, d, s))
+            assert r.dtype == np.int64 and len(r) == cnt and rsha(r)[:16] == h16, (n, d, s)
+
+    def test_configs_1_to_3(self, pkg, golden, gen_mod):
+        for c in ("1", "2", "3"):
+            g = golden["configs"][c]
+            v = gen_mod.config_values(int(c))
+            r = pkg.prime_ranks_from_values(v)
+            assert len(r) == g["primes"] and rsha(r) == g["ranks_sha256"], c
+            r2 = pkg.dense_prime_ranks(pkg.TruthTable(g["n"], gen_mod.values_to_words(v)))
+            assert np.array_equal(r, r2)
+
+    def test_readme_and_dc(self, pkg, golden, gen_mod):
+        for e in golden["readme"]:
+            r = pkg.dense_prime_ranks(tt_of(pkg, gen_mod, e["n"], e["density"], e["seed"]))
+            assert len(r) == e["primes"] and rsha(r) == e["ranks_sha256"]
+        for e in golden["dc_cases"]:
+            r = pkg.prime_ranks_from_values(gen_mod.gen3(e["n"], e["p_on"], e["p_dc"], e["seed"]))
+            assert len(r) == e["primes"] and rsha(r) == e["ranks_sha256"]
+
+    @pytest.mark.parametrize("n", list(range(11, 21)))
+    def test_vs_oracle(self, pkg, oracle_mod, gen_mod, n):
+        for d in (0.0, 0.3, 0.7, 0.95, 1.0):
+            w = gen_mod.random_words(n, d, n)
+            got = pkg.dense_prime_ranks(pkg.TruthTable(n, w))
+            want = oracle_mod.dense_prime_ranks(w, n)
+            assert np.array_equal(got, want), (n, d)
+
+    @pytest.mark.parametrize("n,p_on,p_dc", [(21, 0.75, 0.05), (22, 0.9, 0.05)])
+    def test_vs_oracle_large(self, pkg, oracle_mod, gen_mod, n, p_on, p_dc):
+        v = gen_mod.gen3(n, p_on, p_dc, 3)
+        got = pkg.prime_ranks_from_values(v)
+        want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
+        assert np.array_equal(got, want)
+
+
+class TestBitmap:
+    @pytest.mark.parametrize("n", [5, 6, 9, 12, 13, 15, 17, 19])
+    def test_final_bitmap_equals_reference_state(self, pkg, oracle_mod, gen_mod, n):
+        w = gen_mod.random_words(n, 0.7, 5)
+        st = oracle_mod.OracleState(w, n, 5)
+        st.run_merge_reduce()
+        got = pkg.prime_bitmap(pkg.TruthTable(n, w))
+        assert np.array_equal(got, st.words)
+
+
+class TestContract:
+    def test_split_and_optimized_accepted(self, pkg, gen_mod):
+        tt = tt_of(pkg, gen_mod, 9, 0.5, 21)
+        base = pkg.dense_prime_ranks(tt)
+        for h in range(1, 10):
+            assert np.array_equal(pkg.dense_prime_ranks(tt, h=h), base)
+            assert np.array_equal(pkg.dense_prime_ranks(tt, h=h, optimized=False), base)
+
+    def test_mem_cap_exact(self, pkg):
+        tt = pkg.TruthTable.empty(12)
+        need = pkg.state_bytes(12, 5)
+        with pytest.raises(pkg.ResourceLimitError) as exc:
+            pkg.dense_prime_ranks(tt, h=5, mem_cap=need - 1)
+        assert str(need) in str(exc.value) and "bytes" in str(exc.value)
+        pkg.dense_prime_ranks(tt, h=5, mem_cap=need)  # exactly at the cap is fine
+        with pytest.raises(pkg.ResourceLimitError):
+            pkg.run_engine("dense", pkg.TruthTable.full(14), mem_cap=1000)
+
+    def test_run_engine_and_count(self, pkg, gen_mod):
+        tt = tt_of(pkg, gen_mod, 16, 0.5, 42)
+        r = pkg.run_engine("dense", tt)
+        assert len(r) == 68460  # pkg/README.md:54-55
+        assert pkg.count_primes(tt) == 68460
+
+    def test_repeated_calls_stable(self, pkg, gen_mod):
+        outs = [pkg.dense_prime_ranks(tt_of(pkg, gen_mod, 18, 0.8, 1)) for _ in range(3)]
+        assert all(np.array_equal(outs[0], o) for o in outs[1:])
+        small = pkg.dense_prime_ranks(tt_of(pkg, gen_mod, 7, 0.5, 2))
+        again = pkg.dense_prime_ranks(tt_of(pkg, gen_mod, 18, 0.8, 1))
+        assert np.array_equal(outs[0], again) and len(small) > 0
+
+
+class TestDevice:
+    def test_gen3_device_matches_oracle(self, pkg, gen_mod):
+        from paper_2302_10083_b200 import device
+
+        for n, pon, pdc, s in ((16, 0.9, 0.05, 1), (20, 0.75, 0.05, 3), (12, 0.5, 0.0, 0)):
+            v = device.gen3_device(n, pon, pdc, s).cpu().numpy()
+            assert np.array_equal(v, gen_mod.gen3(n, pon, pdc, s))
+
+    def test_device_entry_point(self, pkg, golden, gen_mod):
+        import torch
+
+        from paper_2302_10083_b200 import device
+
+        g = golden["configs"]["2"]
+        v = device.gen3_device(16, 0.90, 0.05, 1)
+        r, cnt = device.dense_prime_ranks_device(v, 16)
+        assert cnt == g["primes"] and rsha(r.cpu().numpy()) == g["ranks_sha256"]
+        words = torch.from_numpy(gen_mod.values_to_words(gen_mod.config_values(2)).view(np.int64)).cuda()
+        r2, cnt2 = device.dense_prime_ranks_device(words, 16)
+        assert cnt2 == cnt and torch.equal(r, r2)
+        _, c3 = device.dense_prime_ranks_device(v, 16, count_only=True)
+        assert c3 == cnt
+
+
+@pytest.mark.slow
+class TestFullSize:
+    def test_config4_n24(self, pkg, golden, oracle_mod, gen_mod):
+        """BASELINE config 4 at full size: pinned by the reference's count and hash."""
+        from paper_2302_10083_b200 import device
+
+        g = golden["configs"]["4"]
+        v = device.gen3_device(24, 0.75, 0.05, 3)
+        r, cnt = device.dense_prime_ranks_device(v, 24)
+        host = r.cpu().numpy()
+        assert cnt == g["primes"]
+        assert rsha(host)[:16] == g["ranks_sha256_prefix"]
+        assert host[:3].tolist() == g["first"] and host[-3:].tolist() == g["last"]
+        assert np.all(np.diff(host) > 0)  # unique, ascending
+        # independent implicant + maximality check on sampled primes
+        on = gen_mod.config_values(4) != 0
+        rng = np.random.default_rng(7)
+        for r0 in rng.choice(host, 200, replace=False):
+            imp, mx = oracle_mod.is_prime_cube(int(r0), 24, on)
+            assert imp and mx, int(r0)
+        # and through the host API (same arrays)
+        hr = pkg.prime_ranks_from_values(v.cpu().numpy())
+        assert np.array_equal(hr, host)
