@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the dense prime-implicant path (BASELINE.json metric).
+
+Metric: ternary cells per second, 3^n / t, for "all prime implicants at n"
+(BASELINE.json `metric`). Workload at N=1: BASELINE config 4 — n=24, 2^24
+uint8 values i.i.d. P(on)=0.75, P(dc)=0.05, rest off, seed 3; the largest
+configuration that fits one GPU (config 5, n=27, needs 1 TB). Seeded synthetic
+inputs from the reference's frozen generator.
+
+  value  device-resident: the uint8 table is generated in HBM before the
+         timed region; a step = the whole engine (pack, merge passes, reduce
+         passes, compaction of all prime ranks into an HBM int64 buffer).
+  e2e    the public API a user calls (prime_ranks_from_values) with a pinned
+         host input and the int64 rank array returned on the host: H2D of the
+         table and D2H of every rank inside each timed step.
+  roofline  the dominant kernel's algorithmic bytes per launch / its
+         CUDA-event duration vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the oracle port (C restatement of the reference's dense
+         engine, all host threads) on a bounded sample of the same workload.
+
+--impl reference times that CPU implementation alone (the reference arm).
+Under torchrun (N>1) the engine runs sharded on the top log2(N) variables
+(paper_2302_10083_b200.sharded); the reference arm runs on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOAD = dict(n=24, p_on=0.75, p_dc=0.05, seed=3)  # BASELINE config 4
+METRIC = "ternary cells/s to all prime implicants"
+UNIT = "cells/s"
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak_gbs():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = (
+        "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+        "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+        "clocks_event_reasons.sw_power_cap"
+    )
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                    capture_output=True,
+                    text=True,
+                    timeout=5,
+                ).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": reasons,
+            "samples": len(self.samples),
+        }
+
+
+def cpu_port_run(n: int, threads: int = 0) -> tuple[float, int, int]:
+    """Oracle port (C restatement of dense.py) on the host cores: (seconds, primes, threads)."""
+    from oracle import gen as G
+    from oracle import oracle as O
+
+    O.build()
+    t = O.set_threads(threads if threads > 0 else (os.cpu_count() or 1))
+    w = G.values_to_words(G.gen3(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"]))
+    t0 = time.perf_counter()
+    r = O.dense_prime_ranks(w, n)
+    dt = time.perf_counter() - t0
+    return dt, len(r), t
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return 0
+    n_s = args.cpu_sample_n
+    for _ in range(args.warmup):
+        cpu_port_run(n_s)
+    times, cnt, thr = [], 0, 1
+    for _ in range(args.steps):
+        dt, cnt, thr = cpu_port_run(n_s)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = 3**n_s / t
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded frozen generator, SURVEY.md §8(d))",
+        "config": {"workload": "BASELINE config 4 (n=24, p_on=0.75, p_dc=0.05, seed=3)", "sample_n": n_s},
+        "cpu_baseline": {
+            "value": value,
+            "unit": UNIT,
+            "cores": thr,
+            "kind": "port",
+            "sample": f"n={n_s} of the config-4 distribution ({3**n_s} cells, {cnt} primes) per step",
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get("kernels", {}).get(kernel)
+        if e and e.get("n") == WORKLOAD["n"]:
+            return e.get("dram_bytes")
+    except Exception:
+        pass
+    return None
+
+
+def run_engine_bench(args):
+    import torch
+
+    from paper_2302_10083_b200 import _lib, device
+    import paper_2302_10083_b200 as pkg
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    n = args.n
+    if world > 1:
+        from paper_2302_10083_b200 import sharded
+
+        return sharded.bench_main(args, WORKLOAD, METRIC, UNIT)
+
+    dev = torch.device(f"cuda:{local}")
+    values = device.gen3_device(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"], device=local)
+    torch.cuda.synchronize()
+    # size the device output once (untimed)
+    out = torch.empty(1, dtype=torch.int64, device=dev)
+    r, cnt = device.dense_prime_ranks_device(values, n, out=None)
+    out = torch.empty(int(cnt * 1.02) + 1024, dtype=torch.int64, device=dev)
+    del r
+    for _ in range(args.warmup):
+        device.dense_prime_ranks_device(values, n, out=out)
+    torch.cuda.synchronize()
+
+    # ---- value: device-resident, CUDA events on the launching stream
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    pass_times: dict[str, list[float]] = {}
+    pass_bytes: dict[str, int] = {}
+    launches = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, c = device.dense_prime_ranks_device(values, n, out=out, timing=True)
+            assert c == cnt
+            tl = _lib.timings()
+            launches += len(tl) + 1  # + the uint8 -> bit packing kernel
+            for name, ms, by in tl:
+                pass_times.setdefault(name, []).append(ms)
+                pass_bytes[name] = by
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    value = 3**n / t_step
+
+    # dominant kernel (largest share of the step)
+    tot = {k: sum(v) for k, v in pass_times.items()}
+    dom = max(tot, key=tot.get)
+    launches_per_step = {k: len(v) / args.steps for k, v in pass_times.items()}
+    dom_ms = tot[dom] / len(pass_times[dom])
+    peak, peak_kind = measured_peak_gbs()
+    achieved = pass_bytes[dom] / (dom_ms / 1e3) / 1e9
+    all_bytes = sum(pass_bytes.values())
+    all_ms = sum(tot.values()) / args.steps
+
+    # ---- e2e: public host API, pinned input, ranks back to the host
+    host_vals = torch.empty(1 << n, dtype=torch.uint8, pin_memory=True)
+    host_vals.copy_(values.cpu())
+    hv = host_vals.numpy()
+    for _ in range(max(1, args.warmup)):
+        res = pkg.prime_ranks_from_values(hv)
+        del res
+    e2e_times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pkg.prime_ranks_from_values(hv)
+        e2e_times.append(time.perf_counter() - t0)
+        assert len(res) == cnt
+        del res
+    t_e2e = sum(e2e_times) / len(e2e_times)
+
+    # ---- CPU baseline: oracle port on a bounded sample (rank 0, N=1)
+    cpu = None
+    if not args.no_cpu:
+        dt, ccnt, thr = cpu_port_run(args.cpu_sample_n)
+        cpu = {
+            "value": 3**args.cpu_sample_n / dt,
+            "unit": UNIT,
+            "cores": thr,
+            "kind": "port",
+            "sample": f"n={args.cpu_sample_n} of the config-4 distribution ({3**args.cpu_sample_n} cells, {ccnt} primes), one run",
+        }
+
+    traffic = load_ncu_traffic(dom)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded frozen generator, SURVEY.md §8(d)); generated on device",
+        "config": {
+            "workload": "BASELINE config 4: n=24, P(on)=0.75, P(dc)=0.05, seed 3, all primes as int64 ranks",
+            "n": n,
+            "cells": 3**n,
+            "primes": cnt,
+            "state_bytes": pkg.state_bytes(n, 5),
+            "l2": "no flush needed: the 37 GB state is far larger than the 126 MB L2",
+            "plan": _lib.plan(n),
+        },
+        "e2e": {
+            "value": 3**n / t_e2e,
+            "unit": UNIT,
+            "ms_per_step": t_e2e * 1e3,
+            "h2d_bytes_per_step": int(1 << n),
+            "d2h_bytes_per_step": int(cnt * 8 + 8),
+            "api": "paper_2302_10083_b200.prime_ranks_from_values (C ABI dqmc_primes_u8)",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": dom,
+            "achieved": achieved,
+            "peak": peak,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": pass_bytes[dom],
+            "ms_per_launch": dom_ms,
+        },
+        "passes": {
+            k: {"ms": tot[k] / len(pass_times[k]), "bytes": pass_bytes[k],
+                "gbs": pass_bytes[k] / (tot[k] / len(pass_times[k]) / 1e3) / 1e9,
+                "launches_per_step": launches_per_step[k]}
+            for k in tot
+        },
+        "all_passes_gbs": all_bytes / (all_ms / 1e3) / 1e9,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--cpu-sample-n", type=int, default=21)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine_bench(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -812,6 +812,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
     int64_t total = 0;
     CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (fa.ranks && !tm.bytes.empty()) tm.bytes.back() += (uint64_t)std::min<int64_t>(total, cap) * 8;
     tm.finish();
     *count = total;
     g_eng.state_n = keep ? p.n : -1;
