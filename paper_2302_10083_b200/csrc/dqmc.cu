@@ -17,7 +17,9 @@
 //                          warp-aggregated popcount, decoupled look-back scan
 //                          and ordered compaction to int64 ranks.
 // Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -181,46 +183,55 @@ constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 // In-block reduce, popcount, decoupled look-back and ordered compaction of one
 // tile (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order
-// is rank order, so the output needs no sort).
-__device__ void tile_finish(uint32_t *sm, int g, int64_t tile, int64_t blk0, const FinalArgs &fa) {
+// is rank order, so the output needs no sort). Warp w owns the contiguous
+// block range [b0, b1); lane l takes blocks b0+l, b0+l+32, ... for the
+// in-block axes and the popcount, then the same range word-by-word (lane =
+// word) for the ordered emission, which skips all-zero word groups.
+__device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
+    constexpr int kMaxIter = 16;  // ceil(max warp range / 32); ranges are <= 274 blocks for 3^7
     __shared__ int64_t s_warp_off[kTileThreads / 32];
+    __shared__ uint32_t s_nz[kTileThreads / 32][kMaxIter];
     __shared__ int64_t s_tile_off;
-    const int nb = (int)pow3l(g);
-    const int nwords = nb * 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
+    const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
+    const int nj = (b1 - b0 + 31) >> 5;
 
-    // (1) in-block axes, thread per block
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        uint32_t v[8];
-        uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
-        const uint4 x0 = p[0], x1 = p[1];
-        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-        if (fa.ib_mask) inblock_reduce(v, fa.ib_mask);
-        const uint4 y0 = make_uint4(v[0], v[1], v[2], v[3]);
-        const uint4 y1 = make_uint4(v[4], v[5], v[6], v[7]);
-        p[0] = y0;
-        p[1] = y1;
-        if (fa.bitmap_out) {
-            uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
-            q[0] = y0;
-            q[1] = y1;
-        }
-    }
-    __syncthreads();
-
-    // (2) warp-chunked counts: warp w owns words [w0, w1)
-    const int per = (nwords + nwarps - 1) / nwarps;
-    const int w0 = min(nwords, warp * per), w1 = min(nwords, w0 + per);
+    // (1) in-block axes + count; ballot of nonzero blocks per 32-block group
     int cnt = 0;
-    for (int i = w0 + lane; i < w1; i += 32) cnt += __popc(sm[i]);
+    for (int j = 0; j < nj; j++) {
+        const int b = b0 + 32 * j + lane;
+        uint32_t nzb = 0;
+        if (b < b1) {
+            uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+            uint4 x0 = p[0], x1 = p[1];
+            if (fa.ib_mask) {
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, fa.ib_mask);
+                x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                p[0] = x0;
+                p[1] = x1;
+            }
+            if (fa.bitmap_out) {
+                uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+                q[0] = x0;
+                q[1] = x1;
+            }
+            const int c = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) +
+                          __popc(x1.y) + __popc(x1.z) + __popc(x1.w);
+            cnt += c;
+            nzb = c != 0;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, nzb);
+        if (lane == 0) s_nz[warp][j] = m;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) s_warp_off[warp] = cnt;
     __syncthreads();
 
-    // (3) tile prefix: exclusive scan over warps + decoupled look-back
+    // (2) tile prefix: exclusive scan over warps + decoupled look-back
     if (threadIdx.x == 0) {
         int64_t acc = 0;
         for (int w = 0; w < nwarps; w++) {
@@ -232,11 +243,9 @@ __device__ void tile_finish(uint32_t *sm, int g, int64_t tile, int64_t blk0, con
         int64_t excl = 0;
         volatile unsigned long long *flags = fa.flags;
         if (tile == 0) {
-            __threadfence();
             flags[0] = kFlagInc | (unsigned long long)agg;
         } else {
             flags[tile] = kFlagAgg | (unsigned long long)agg;
-            __threadfence();
             int64_t p = tile - 1;
             while (true) {
                 const unsigned long long f = flags[p];
@@ -246,7 +255,6 @@ __device__ void tile_finish(uint32_t *sm, int g, int64_t tile, int64_t blk0, con
                 if (st == kFlagInc) break;
                 p--;
             }
-            __threadfence();
             flags[tile] = kFlagInc | (unsigned long long)(excl + agg);
         }
         if (tile == fa.ntiles - 1) *fa.total = excl + agg;
@@ -255,27 +263,112 @@ __device__ void tile_finish(uint32_t *sm, int g, int64_t tile, int64_t blk0, con
     __syncthreads();
     if (fa.ranks == nullptr) return;
 
-    // (4) ordered emission: lane = word, warp-inclusive scan of popcounts
+    // (3) ordered emission over nonzero blocks only: four blocks per step,
+    //     lane = (block slot g, word k); warp-inclusive scan of popcounts
     int64_t off = s_tile_off + s_warp_off[warp];
-    for (int base = w0; base < w1; base += 32) {
-        const int i = base + lane;
-        uint32_t w = (i < w1) ? sm[i] : 0u;
-        const int c = __popc(w);
-        int incl = c;
+    const int g = lane >> 3, k = lane & 7;
+    for (int j = 0; j < nj; j++) {
+        uint32_t mask = s_nz[warp][j];
+        while (mask) {
+            uint32_t mm = mask;
+            for (int t = 0; t < g; t++) mm &= mm - 1;
+            uint32_t w = 0;
+            int64_t rank0 = 0;
+            if (mm) {
+                const int blk = b0 + 32 * j + __ffs(mm) - 1;
+                w = sm[blk * 8 + k];
+                rank0 = (blk0 + blk) * 243 + (int64_t)k * 32 - fa.rank_sub;
+            }
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            for (int t = 0; t < 4; t++) mask &= mask - 1;
+            const int c = __popc(w);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int64_t pos = off + incl - c;
+            while (w) {
+                const int b = __ffs(w) - 1;
+                w &= w - 1;
+                if (pos < fa.cap) fa.ranks[pos] = rank0 + b;
+                pos++;
+            }
+            off += __shfl_sync(0xffffffffu, incl, 31);
         }
-        int64_t pos = off + incl - c;
-        const int64_t rank0 = (blk0 + (i >> 3)) * 243 + (int64_t)(i & 7) * 32 - fa.rank_sub;
-        while (w) {
-            const int b = __ffs(w) - 1;
-            w &= w - 1;
-            if (pos < fa.cap) fa.ranks[pos] = rank0 + b;
-            pos++;
-        }
-        off += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) with an mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(mbar)),
+        "r"(phase)
+        : "memory");
+}
+
+// REDUCE along C0 axes [J0, J0+K) of a 3^G-block tile, compile-time shape.
+template <int K, int G, int J0>
+__device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
+    constexpr int N = P3<K>::v;
+    constexpr int SJ = pow3i(J0);
+    constexpr int SPAN = SJ * N;
+    constexpr int NHI = pow3i(G) / SPAN;
+    constexpr int NTASK = SJ * NHI * 8;
+    for (int t = threadIdx.x; t < NTASK; t += blockDim.x) {
+        const int w = t & 7, q = t >> 3;
+        const int lo = q % SJ, hi = q / SJ;
+        const int blk = lo + hi * SPAN;
+        uint32_t v[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) v[i] = sm[(blk + i * SJ) * 8 + w];
+        cube_reduce<K>(v);
+#pragma unroll
+        for (int i = 0; i < N; i++) sm[(blk + i * SJ) * 8 + w] = v[i];
+    }
+    __syncthreads();
+}
+
+template <int G, int J0>
+__device__ __forceinline__ void tile_reduce_c0_t(uint32_t *sm) {
+    if constexpr (G - J0 >= 3) {
+        tile_reduce_axes_t<3, G, J0>(sm);
+        tile_reduce_c0_t<G, J0 + 3>(sm);
+    } else if constexpr (G - J0 == 2) {
+        tile_reduce_axes_t<2, G, J0>(sm);
+    } else if constexpr (G - J0 == 1) {
+        tile_reduce_axes_t<1, G, J0>(sm);
     }
 }
 
@@ -316,22 +409,29 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__res
     }
 }
 
-// pass E: one CTA per C0 tile, tiles taken in rank order by ticket
-__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, int g,
-                                                           unsigned int *ticket, FinalArgs fa) {
-    extern __shared__ __align__(16) uint32_t sm[];
+// pass E: one CTA per C0 tile (3^G blocks), tiles taken in rank order by
+// ticket; the tile arrives in shared memory with one TMA bulk copy.
+template <int G>
+__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, unsigned int *ticket,
+                                                           FinalArgs fa) {
+    extern __shared__ __align__(128) uint32_t sm[];
+    __shared__ __align__(8) uint64_t mbar;
     __shared__ int64_t s_tile;
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    constexpr int NB = pow3i(G);
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(ticket, 1u);
+        mbar_init(&mbar, 1);
+    }
     __syncthreads();
     const int64_t tile = s_tile;
-    const int nb = (int)pow3l(g);
-    const int64_t blk0 = tile * nb;
-    const uint4 *src = reinterpret_cast<const uint4 *>(state + blk0 * 8);
-    uint4 *dst = reinterpret_cast<uint4 *>(sm);
-    for (int t = threadIdx.x; t < nb * 2; t += blockDim.x) dst[t] = __ldcs(src + t);
-    __syncthreads();
-    tile_reduce_c0(sm, g);
-    tile_finish(sm, g, tile, blk0, fa);
+    const int64_t blk0 = tile * NB;
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar, NB * 32);
+        bulk_g2s(sm, state + blk0 * 8, NB * 32, &mbar);
+    }
+    mbar_wait(&mbar, 0);
+    tile_reduce_c0_t<G, 0>(sm);
+    tile_finish(sm, NB, tile, blk0, fa);
 }
 
 // n <= 12: the whole problem is one tile; one CTA does A and E.
@@ -339,7 +439,7 @@ __global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restri
     extern __shared__ __align__(16) uint32_t sm[];
     tile_build(sm, tt32, g, 0);
     tile_reduce_c0(sm, g);
-    tile_finish(sm, g, 0, 0, fa);
+    tile_finish(sm, (int)pow3l(g), 0, 0, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -496,6 +596,216 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
 }
 
 // ---------------------------------------------------------------------------
+// Pipelined strided pass (MERGE_REDUCE / REDUCE_ONLY): persistent CTAs, two
+// tile buffers, one producer warp that streams tiles in and out with TMA
+// (3-D tensor map: words x rows x outer; zero-fill / clipping handle the
+// ragged last column) while nine compute warps work on the other buffer.
+// MERGE_REDUCE gathers only the 2^R binary rows (cp.async, 16 B each).
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int c1, int c2, const void *src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
+                 "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *mbar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+__device__ __forceinline__ void bar_compute(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+constexpr int kComputeWarps = 9;
+constexpr int kPipeThreads = (kComputeWarps + 1) * 32;
+
+template <int R1, int R2>
+struct PipeSmem {
+    static constexpr int NR = P3<R1>::v * P3<R2>::v;
+    static constexpr int TILE_WORDS = NR * 32;
+    static constexpr int STAGE_WORDS = (1 << R1) * (1 << R2) * 32;
+    static constexpr int BOXR = NR > 243 ? 243 : NR;  // TMA box rows (<= 256)
+    static constexpr int NBOX = NR / BOXR;
+};
+
+template <int R1, int R2, int MODE>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ state, int64_t Q,
+                   int64_t ncol, int64_t nitems, uint32_t ib_mask) {
+    using SM = PipeSmem<R1, R2>;
+    constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v, B1 = 1 << R1, B2 = 1 << R2;
+    constexpr int NR = SM::NR;
+    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t *tile[2] = {smem, smem + SM::TILE_WORDS};
+    uint32_t *stage[2] = {smem + 2 * SM::TILE_WORDS, smem + 2 * SM::TILE_WORDS + SM::STAGE_WORDS};
+    __shared__ __align__(8) uint64_t full[2], computed[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&full[b], MODE == MERGE_REDUCE ? 32 : 1);
+            mbar_init(&computed[b], kComputeWarps);
+        }
+    }
+    __syncthreads();
+
+    if (warp == kComputeWarps) {
+        // ------------------------------ producer warp
+        for (int64_t i = 0; i < L + 2; i++) {
+            const int b = (int)(i & 1);
+            if (i >= 2) {
+                const int64_t it = blockIdx.x + (i - 2) * gridDim.x;
+                mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
+                if (lane == 0) {
+                    const int c0 = (int)((it % ncol) * 32), c2 = (int)(it / ncol);
+#pragma unroll
+                    for (int x = 0; x < SM::NBOX; x++)
+                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile[b] + x * SM::BOXR * 32);
+                    bulk_commit();
+                    bulk_wait_read0();
+                }
+                __syncwarp();
+            }
+            if (i < L) {
+                const int64_t it = blockIdx.x + i * gridDim.x;
+                const int64_t col = it % ncol, outer = it / ncol;
+                if (MODE == REDUCE_ONLY) {
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
+#pragma unroll
+                        for (int x = 0; x < SM::NBOX; x++)
+                            tma_load_3d(tile[b] + x * SM::BOXR * 32, &tmap, (int)(col * 32), x * SM::BOXR,
+                                        (int)outer, &full[b]);
+                    }
+                } else {
+                    // gather the binary rows: B1*B2 rows x 8 chunks of 16 B
+                    const int64_t c0 = col * kRowBlocks;
+                    const int valid_words = (int)min((int64_t)kRowBlocks, Q - c0) * 8;
+                    for (int t = lane; t < B1 * B2 * 8; t += 32) {
+                        const int ch = t & 7, row = t >> 3;
+                        const int b1 = row % B1, b2 = row / B1;
+                        const int rho = bin_to_tern(b1) + N1 * bin_to_tern(b2);
+                        const bool ok = ch * 4 < valid_words;
+                        const uint32_t *src = state + ((int64_t)rho * Q + c0) * 8 + (ok ? ch * 4 : 0);
+                        cp_async16(stage[b] + row * 32 + ch * 4, src, ok);
+                    }
+                    cp_async_mbar_arrive(&full[b]);
+                }
+            }
+        }
+        if (lane == 0) bulk_wait0();
+        return;
+    }
+
+    // ---------------------------------- compute warps
+    constexpr int NCT = kComputeWarps * 32;
+    for (int64_t i = 0; i < L; i++) {
+        const int b = (int)(i & 1);
+        uint32_t *sm = tile[b];
+        mbar_wait(&full[b], (unsigned)((i >> 1) & 1));
+        if (MODE == MERGE_REDUCE) {
+            const uint32_t *st = stage[b];
+            // round 1: merge the R1 axes for each binary rho2
+            for (int t2 = warp; t2 < B2; t2 += kComputeWarps) {
+                const int r2 = bin_to_tern(t2);
+                uint32_t v[N1];
+#pragma unroll
+                for (int x = 0; x < N1; x++) v[x] = 0;
+#pragma unroll
+                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = st[(b1 + B1 * t2) * 32 + lane];
+                cube_merge<R1>(v);
+                if (R2 == 0) cube_reduce<R1>(v);
+#pragma unroll
+                for (int x = 0; x < N1; x++) sm[(x + N1 * r2) * 32 + lane] = v[x];
+            }
+            if (R2 > 0) {
+                bar_compute(NCT);
+                // round 2: merge + reduce the R2 axes
+                for (int t1 = warp; t1 < N1; t1 += kComputeWarps) {
+                    uint32_t v[N2];
+#pragma unroll
+                    for (int x = 0; x < N2; x++) v[x] = 0;
+#pragma unroll
+                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = sm[(t1 + N1 * bin_to_tern(b2)) * 32 + lane];
+                    cube_merge<R2>(v);
+                    cube_reduce<R2>(v);
+#pragma unroll
+                    for (int x = 0; x < N2; x++) sm[(t1 + N1 * x) * 32 + lane] = v[x];
+                }
+                bar_compute(NCT);
+                // round 3: reduce the R1 axes
+                for (int t2 = warp; t2 < N2; t2 += kComputeWarps) {
+                    uint32_t v[N1];
+#pragma unroll
+                    for (int x = 0; x < N1; x++) v[x] = sm[(x + N1 * t2) * 32 + lane];
+                    cube_reduce<R1>(v);
+#pragma unroll
+                    for (int x = 0; x < N1; x++) sm[(x + N1 * t2) * 32 + lane] = v[x];
+                }
+            }
+        } else {
+            // round 1: reduce the R1 axes
+            for (int t2 = warp; t2 < N2; t2 += kComputeWarps) {
+                uint32_t v[N1];
+#pragma unroll
+                for (int x = 0; x < N1; x++) v[x] = sm[(x + N1 * t2) * 32 + lane];
+                cube_reduce<R1>(v);
+#pragma unroll
+                for (int x = 0; x < N1; x++) sm[(x + N1 * t2) * 32 + lane] = v[x];
+            }
+            if (R2 > 0) {
+                bar_compute(NCT);
+                for (int t1 = warp; t1 < N1; t1 += kComputeWarps) {
+                    uint32_t v[N2];
+#pragma unroll
+                    for (int x = 0; x < N2; x++) v[x] = sm[(t1 + N1 * x) * 32 + lane];
+                    cube_reduce<R2>(v);
+#pragma unroll
+                    for (int x = 0; x < N2; x++) sm[(t1 + N1 * x) * 32 + lane] = v[x];
+                }
+            }
+        }
+        if (ib_mask) {
+            bar_compute(NCT);
+            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+                uint4 *p = reinterpret_cast<uint4 *>(sm + t * 8);
+                const uint4 x0 = p[0], x1 = p[1];
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, ib_mask);
+                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&computed[b]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 struct Plan {
@@ -588,6 +898,8 @@ struct Engine {
     std::vector<uint64_t> pass_bytes;
     int state_n = -1;  // n whose final bitmap is held in `state` (KEEP_BITMAP)
     bool attrs_set = false;
+    int num_sms = 148;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
 };
 
 Engine g_eng;
@@ -636,6 +948,26 @@ int set_strided_attr() {
     return DQMC_OK;
 }
 
+template <int R1, int R2, int MODE>
+int set_pipe_attr() {
+    using SM = PipeSmem<R1, R2>;
+    constexpr int smem = (2 * SM::TILE_WORDS + 2 * SM::STAGE_WORDS) * 4;
+    CK(cudaFuncSetAttribute(k_strided_pipe<R1, R2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return DQMC_OK;
+}
+
+template <int MODE>
+int set_pipe_attrs() {
+    int rc;
+    if ((rc = set_pipe_attr<1, 0, MODE>())) return rc;
+    if ((rc = set_pipe_attr<2, 0, MODE>())) return rc;
+    if ((rc = set_pipe_attr<3, 0, MODE>())) return rc;
+    if ((rc = set_pipe_attr<2, 2, MODE>())) return rc;
+    if ((rc = set_pipe_attr<3, 2, MODE>())) return rc;
+    if ((rc = set_pipe_attr<3, 3, MODE>())) return rc;
+    return DQMC_OK;
+}
+
 template <int MODE>
 int set_mode_attrs() {
     int rc;
@@ -652,12 +984,15 @@ int ensure_attrs() {
     if (g_eng.attrs_set) return DQMC_OK;
     const int tile_smem = (int)pow3l(kC0Max) * 32;
     CK(cudaFuncSetAttribute(k_c0_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
-    CK(cudaFuncSetAttribute(k_c0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     int rc;
     if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;
     if ((rc = set_mode_attrs<MERGE_REDUCE>())) return rc;
     if ((rc = set_mode_attrs<REDUCE_ONLY>())) return rc;
+    if ((rc = set_pipe_attrs<MERGE_REDUCE>())) return rc;
+    if ((rc = set_pipe_attrs<REDUCE_ONLY>())) return rc;
+    CK(cudaDeviceGetAttribute(&g_eng.num_sms, cudaDevAttrMultiProcessorCount, g_eng.device));
     g_eng.attrs_set = true;
     return DQMC_OK;
 }
@@ -701,6 +1036,54 @@ struct Timer {
         ev.clear();
     }
 };
+
+// 3-D tensor map over the state for a strided group: dim0 = words of the
+// inner extent (8*Q), dim1 = the 3^R rows (stride Q blocks), dim2 = outer
+// index (stride 3^R*Q blocks); box = 32 words x BOXR rows x 1.
+int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr) {
+    if (!g_eng.encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        g_eng.encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)(8 * Q), (cuuint64_t)nr, (cuuint64_t)nouter};
+    cuuint64_t strides[2] = {(cuuint64_t)(Q * 32), (cuuint64_t)(Q * 32 * nr)};
+    cuuint32_t box[3] = {32, (cuuint32_t)boxr, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_eng.encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, state, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return DQMC_OK;
+}
+
+template <int R1, int R2, int MODE>
+int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
+    using SM = PipeSmem<R1, R2>;
+    CUtensorMap map;
+    int rc;
+    if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR))) return rc;
+    const int64_t nitems = ncol * nouter;
+    const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
+    constexpr int smem = (2 * SM::TILE_WORDS + 2 * SM::STAGE_WORDS) * 4;
+    k_strided_pipe<R1, R2, MODE><<<grid, kPipeThreads, smem, s>>>(map, state, Q, ncol, nitems, ib);
+    CK(cudaGetLastError());
+    return DQMC_OK;
+}
+
+template <int MODE>
+int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
+    switch (r) {
+        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, s);
+        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, s);
+        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, s);
+        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, s);
+        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, s);
+        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, s);
+    }
+}
 
 template <int MODE>
 void launch_strided_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nitems, uint32_t ib,
@@ -784,8 +1167,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
             const int k = p.m - 1;
             const int64_t Q = pow3l(p.a[k]);
             const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
-            launch_strided_mode<MERGE_REDUCE>(p.r[k], g_eng.state, Q, ncol, ncol, p.ib_C, s);
-            CK(cudaGetLastError());
+            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], g_eng.state, Q, ncol, 1, p.ib_C, s))) return rc;
             tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(frac(p.r[k]) + S));
         }
         // passes D: reduce the other groups
@@ -794,9 +1176,8 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
             const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
             int above = 0;
             for (int j = k + 1; j < p.m; j++) above += p.r[j];
-            const int64_t nitems = ncol * pow3l(above);
-            launch_strided_mode<REDUCE_ONLY>(p.r[k], g_eng.state, Q, ncol, nitems, p.ib_D[k], s);
-            CK(cudaGetLastError());
+            if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], g_eng.state, Q, ncol, pow3l(above), p.ib_D[k], s)))
+                return rc;
             tm.mark("k_strided<REDUCE>", 2 * S);
         }
         // pass E
@@ -805,7 +1186,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
         CK(cudaMemsetAsync(g_eng.flags, 0, (size_t)ntiles * 8, s));
         fa.ib_mask = p.ib_E;
         fa.ntiles = ntiles;
-        k_c0_final<<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, p.g, g_eng.ticket, fa);
+        k_c0_final<kC0Max><<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, g_eng.ticket, fa);
         CK(cudaGetLastError());
         tm.mark("k_c0_final", S + (keep ? S : 0));
     }
