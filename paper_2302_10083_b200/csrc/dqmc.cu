@@ -41,7 +41,7 @@ constexpr int kC0Max = 7;        // block axes in the contiguous tile (3^7 block
 constexpr int kGroupMax = 6;     // block axes per strided pass (3^6 rows x 128 B = 91 KiB)
 constexpr int kRowBlocks = 4;    // blocks per strided row (128 B)
 constexpr int kStridedThreads = 288;  // 9 warps: 27 sub-cube tasks per round divide evenly
-constexpr int kTileThreads = 256;
+constexpr int kTileThreads = 224;  // 7 warps: the 4+3 C0 rounds divide into 1 and 3 tasks/thread
 
 enum Mode { MERGE_ONLY = 0, MERGE_REDUCE = 1, REDUCE_ONLY = 2 };
 
@@ -188,114 +188,129 @@ constexpr unsigned long long kValMask = (1ull << 62) - 1;
 // in-block axes and the popcount, then the same range word-by-word (lane =
 // word) for the ordered emission, which skips all-zero word groups.
 __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
-    constexpr int kMaxIter = 16;  // ceil(max warp range / 32); ranges are <= 274 blocks for 3^7
+    constexpr int kMaxIter = 12;  // ceil(max warp range / 32): 3^7 blocks over 7 warps = 313 blocks
     __shared__ int64_t s_warp_off[kTileThreads / 32];
-    __shared__ uint32_t s_nz[kTileThreads / 32][kMaxIter];
     __shared__ int64_t s_tile_off;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
     const int nj = (b1 - b0 + 31) >> 5;
+    const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
 
-    // (1) in-block axes + count; ballot of nonzero blocks per 32-block group
+    // (1) lane = block: in-block axes (if any left for this pass) + popcount
+    int cj[kMaxIter];
     int cnt = 0;
-    for (int j = 0; j < nj; j++) {
-        const int b = b0 + 32 * j + lane;
-        uint32_t nzb = 0;
-        if (b < b1) {
-            uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
-            uint4 x0 = p[0], x1 = p[1];
-            if (fa.ib_mask) {
-                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                inblock_reduce(v, fa.ib_mask);
-                x0 = make_uint4(v[0], v[1], v[2], v[3]);
-                x1 = make_uint4(v[4], v[5], v[6], v[7]);
-                p[0] = x0;
-                p[1] = x1;
-            }
-            if (fa.bitmap_out) {
-                uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
-                q[0] = x0;
-                q[1] = x1;
-            }
-            const int c = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) +
-                          __popc(x1.y) + __popc(x1.z) + __popc(x1.w);
-            cnt += c;
-            nzb = c != 0;
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, nzb);
-        if (lane == 0) s_nz[warp][j] = m;
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) s_warp_off[warp] = cnt;
+    for (int j = 0; j < kMaxIter; j++) {
+        cj[j] = 0;
+        if (j < nj) {
+            const int b = b0 + 32 * j + lane;
+            if (b < b1) {
+                uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                if (fa.ib_mask) {
+                    uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    inblock_reduce(v, fa.ib_mask);
+                    x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                    x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                    p[h] = h ? x1 : x0;
+                    p[h ^ 1] = h ? x0 : x1;
+                }
+                if (fa.bitmap_out) {
+                    uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+                    q[0] = x0;
+                    q[1] = x1;
+                }
+                cj[j] = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
+                        __popc(x1.z) + __popc(x1.w);
+                cnt += cj[j];
+            }
+        }
+    }
+    int wsum = cnt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (lane == 0) s_warp_off[warp] = wsum;
     __syncthreads();
 
-    // (2) tile prefix: exclusive scan over warps + decoupled look-back
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        for (int w = 0; w < nwarps; w++) {
-            const int64_t c = s_warp_off[w];
-            s_warp_off[w] = acc;
-            acc += c;
+    // (2) tile prefix: exclusive scan over warps + decoupled look-back done by
+    //     warp 0, 32 predecessors per step (one flag word each: status|value)
+    if (warp == 0) {
+        int64_t agg = 0;
+        if (lane == 0) {
+            int64_t acc = 0;
+            for (int w = 0; w < nwarps; w++) {
+                const int64_t c = s_warp_off[w];
+                s_warp_off[w] = acc;
+                acc += c;
+            }
+            agg = acc;
         }
-        const int64_t agg = acc;
-        int64_t excl = 0;
+        agg = __shfl_sync(0xffffffffu, agg, 0);
         volatile unsigned long long *flags = fa.flags;
+        int64_t excl = 0;
         if (tile == 0) {
-            flags[0] = kFlagInc | (unsigned long long)agg;
+            if (lane == 0) flags[0] = kFlagInc | (unsigned long long)agg;
         } else {
-            flags[tile] = kFlagAgg | (unsigned long long)agg;
+            if (lane == 0) flags[tile] = kFlagAgg | (unsigned long long)agg;
             int64_t p = tile - 1;
             while (true) {
-                const unsigned long long f = flags[p];
+                const int64_t q = p - lane;
+                const unsigned long long f = q >= 0 ? flags[q] : (2ull << 62);
                 const unsigned long long st = f & ~kValMask;
-                if (st == 0) continue;  // predecessor still running (it holds an earlier ticket)
-                excl += (int64_t)(f & kValMask);
-                if (st == kFlagInc) break;
-                p--;
+                if (__any_sync(0xffffffffu, st == 0)) continue;  // a predecessor is still counting
+                const unsigned incm = __ballot_sync(0xffffffffu, st == kFlagInc);
+                const int first = incm ? __ffs(incm) - 1 : 32;
+                int64_t v = lane <= first ? (int64_t)(f & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (incm) break;
+                p -= 32;
             }
-            flags[tile] = kFlagInc | (unsigned long long)(excl + agg);
+            if (lane == 0) flags[tile] = kFlagInc | (unsigned long long)(excl + agg);
         }
-        if (tile == fa.ntiles - 1) *fa.total = excl + agg;
-        s_tile_off = excl;
+        if (lane == 0) {
+            if (tile == fa.ntiles - 1) *fa.total = excl + agg;
+            s_tile_off = excl;
+        }
     }
     __syncthreads();
     if (fa.ranks == nullptr) return;
 
-    // (3) ordered emission over nonzero blocks only: four blocks per step,
-    //     lane = (block slot g, word k); warp-inclusive scan of popcounts
+    // (3) ordered emission, lane = block: warp-inclusive scan of the block
+    //     counts kept from (1); only nonzero blocks are re-read.
     int64_t off = s_tile_off + s_warp_off[warp];
-    const int g = lane >> 3, k = lane & 7;
-    for (int j = 0; j < nj; j++) {
-        uint32_t mask = s_nz[warp][j];
-        while (mask) {
-            uint32_t mm = mask;
-            for (int t = 0; t < g; t++) mm &= mm - 1;
-            uint32_t w = 0;
-            int64_t rank0 = 0;
-            if (mm) {
-                const int blk = b0 + 32 * j + __ffs(mm) - 1;
-                w = sm[blk * 8 + k];
-                rank0 = (blk0 + blk) * 243 + (int64_t)k * 32 - fa.rank_sub;
-            }
 #pragma unroll
-            for (int t = 0; t < 4; t++) mask &= mask - 1;
-            const int c = __popc(w);
-            int incl = c;
+    for (int j = 0; j < kMaxIter; j++) {
+        if (j < nj) {
+            const int c = cj[j];
+            if (__ballot_sync(0xffffffffu, c != 0) != 0u) {
+                int incl = c;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (c) {
+                    int64_t pos = off + incl - c;
+                    const int b = b0 + 32 * j + lane;
+                    const int64_t base = (blk0 + b) * 243 - fa.rank_sub;
+                    const uint32_t *wp = sm + b * 8;
+#pragma unroll 1
+                    for (int k = 0; k < 8; k++) {
+                        uint32_t w = wp[k];
+                        while (w) {
+                            const int bit = __ffs(w) - 1;
+                            w &= w - 1;
+                            if (pos < fa.cap) fa.ranks[pos] = base + k * 32 + bit;
+                            pos++;
+                        }
+                    }
+                }
+                off += __shfl_sync(0xffffffffu, incl, 31);
             }
-            int64_t pos = off + incl - c;
-            while (w) {
-                const int b = __ffs(w) - 1;
-                w &= w - 1;
-                if (pos < fa.cap) fa.ranks[pos] = rank0 + b;
-                pos++;
-            }
-            off += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
 }
@@ -362,7 +377,10 @@ __device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
 
 template <int G, int J0>
 __device__ __forceinline__ void tile_reduce_c0_t(uint32_t *sm) {
-    if constexpr (G - J0 >= 3) {
+    if constexpr (G - J0 == 7) {
+        tile_reduce_axes_t<4, G, J0>(sm);
+        tile_reduce_c0_t<G, J0 + 4>(sm);
+    } else if constexpr (G - J0 >= 3) {
         tile_reduce_axes_t<3, G, J0>(sm);
         tile_reduce_c0_t<G, J0 + 3>(sm);
     } else if constexpr (G - J0 == 2) {
@@ -638,165 +656,171 @@ __device__ __forceinline__ void bar_compute(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-constexpr int kComputeWarps = 9;
-constexpr int kPipeThreads = (kComputeWarps + 1) * 32;
-
 template <int R1, int R2>
 struct PipeSmem {
-    static constexpr int NR = P3<R1>::v * P3<R2>::v;
+    static constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v;
+    static constexpr int NR = N1 * N2;
     static constexpr int TILE_WORDS = NR * 32;
     static constexpr int STAGE_WORDS = (1 << R1) * (1 << R2) * 32;
     static constexpr int BOXR = NR > 243 ? 243 : NR;  // TMA box rows (<= 256)
     static constexpr int NBOX = NR / BOXR;
+    // one register sub-cube task per compute warp per round
+    static constexpr int CW = (N1 > N2 ? N1 : N2) < 4 ? 4 : (N1 > N2 ? N1 : N2);
+    static constexpr int THREADS = (CW + 1) * 32;
+    static constexpr int SMEM = (2 * TILE_WORDS + 2 * STAGE_WORDS) * 4;
 };
 
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 template <int R1, int R2, int MODE>
-__global__ void __launch_bounds__(kPipeThreads, 1)
-    k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ state, int64_t Q,
+__global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
+    k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
                    int64_t ncol, int64_t nitems, uint32_t ib_mask) {
     using SM = PipeSmem<R1, R2>;
-    constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v, B1 = 1 << R1, B2 = 1 << R2;
+    constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
+    constexpr int CW = SM::CW;
     extern __shared__ __align__(128) uint32_t smem[];
-    uint32_t *tile[2] = {smem, smem + SM::TILE_WORDS};
-    uint32_t *stage[2] = {smem + 2 * SM::TILE_WORDS, smem + 2 * SM::TILE_WORDS + SM::STAGE_WORDS};
     __shared__ __align__(8) uint64_t full[2], computed[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
-            mbar_init(&full[b], MODE == MERGE_REDUCE ? 32 : 1);
-            mbar_init(&computed[b], kComputeWarps);
+            mbar_init(&full[b], 1);
+            mbar_init(&computed[b], CW);
         }
     }
     __syncthreads();
 
-    if (warp == kComputeWarps) {
-        // ------------------------------ producer warp
-        for (int64_t i = 0; i < L + 2; i++) {
-            const int b = (int)(i & 1);
-            if (i >= 2) {
-                const int64_t it = blockIdx.x + (i - 2) * gridDim.x;
-                mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
-                if (lane == 0) {
+    if (warp == CW) {
+        // ------------------------------ producer warp (one elected lane)
+        if (lane == 0) {
+            for (int64_t i = 0; i < L + 2; i++) {
+                const int b = (int)(i & 1);
+                uint32_t *tile = smem + b * SM::TILE_WORDS;
+                if (i >= 2) {
+                    const int64_t it = blockIdx.x + (i - 2) * gridDim.x;
+                    mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
                     const int c0 = (int)((it % ncol) * 32), c2 = (int)(it / ncol);
 #pragma unroll
                     for (int x = 0; x < SM::NBOX; x++)
-                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile[b] + x * SM::BOXR * 32);
+                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile + x * SM::BOXR * 32);
                     bulk_commit();
                     bulk_wait_read0();
                 }
-                __syncwarp();
-            }
-            if (i < L) {
-                const int64_t it = blockIdx.x + i * gridDim.x;
-                const int64_t col = it % ncol, outer = it / ncol;
-                if (MODE == REDUCE_ONLY) {
-                    if (lane == 0) {
+                if (i < L) {
+                    const int64_t it = blockIdx.x + i * gridDim.x;
+                    const int c0 = (int)((it % ncol) * 32), outer = (int)(it / ncol);
+                    if (MODE == REDUCE_ONLY) {
                         mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
 #pragma unroll
                         for (int x = 0; x < SM::NBOX; x++)
-                            tma_load_3d(tile[b] + x * SM::BOXR * 32, &tmap, (int)(col * 32), x * SM::BOXR,
-                                        (int)outer, &full[b]);
+                            tma_load_3d(tile + x * SM::BOXR * 32, &tmap, c0, x * SM::BOXR, outer, &full[b]);
+                    } else {
+                        // binary rows: one 5-D box {32 words, 2, .., 2} per binary rho2
+                        uint32_t *st = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
+                        mbar_expect_tx(&full[b], SM::STAGE_WORDS * 4);
+#pragma unroll
+                        for (int b2 = 0; b2 < B2; b2++)
+                            tma_load_5d(st + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
                     }
-                } else {
-                    // gather the binary rows: B1*B2 rows x 8 chunks of 16 B
-                    const int64_t c0 = col * kRowBlocks;
-                    const int valid_words = (int)min((int64_t)kRowBlocks, Q - c0) * 8;
-                    for (int t = lane; t < B1 * B2 * 8; t += 32) {
-                        const int ch = t & 7, row = t >> 3;
-                        const int b1 = row % B1, b2 = row / B1;
-                        const int rho = bin_to_tern(b1) + N1 * bin_to_tern(b2);
-                        const bool ok = ch * 4 < valid_words;
-                        const uint32_t *src = state + ((int64_t)rho * Q + c0) * 8 + (ok ? ch * 4 : 0);
-                        cp_async16(stage[b] + row * 32 + ch * 4, src, ok);
-                    }
-                    cp_async_mbar_arrive(&full[b]);
                 }
             }
+            bulk_wait0();
         }
-        if (lane == 0) bulk_wait0();
         return;
     }
 
     // ---------------------------------- compute warps
-    constexpr int NCT = kComputeWarps * 32;
+    constexpr int NCT = CW * 32;
     for (int64_t i = 0; i < L; i++) {
         const int b = (int)(i & 1);
-        uint32_t *sm = tile[b];
+        const int tb = b * SM::TILE_WORDS;
         mbar_wait(&full[b], (unsigned)((i >> 1) & 1));
         if (MODE == MERGE_REDUCE) {
-            const uint32_t *st = stage[b];
+            const int sb = 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
             // round 1: merge the R1 axes for each binary rho2
-            for (int t2 = warp; t2 < B2; t2 += kComputeWarps) {
+            for (int t2 = warp; t2 < B2; t2 += CW) {
                 const int r2 = bin_to_tern(t2);
                 uint32_t v[N1];
 #pragma unroll
                 for (int x = 0; x < N1; x++) v[x] = 0;
 #pragma unroll
-                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = st[(b1 + B1 * t2) * 32 + lane];
+                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * 32 + lane];
                 cube_merge<R1>(v);
                 if (R2 == 0) cube_reduce<R1>(v);
 #pragma unroll
-                for (int x = 0; x < N1; x++) sm[(x + N1 * r2) * 32 + lane] = v[x];
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * 32 + lane] = v[x];
             }
             if (R2 > 0) {
                 bar_compute(NCT);
                 // round 2: merge + reduce the R2 axes
-                for (int t1 = warp; t1 < N1; t1 += kComputeWarps) {
+                for (int t1 = warp; t1 < N1; t1 += CW) {
                     uint32_t v[N2];
 #pragma unroll
                     for (int x = 0; x < N2; x++) v[x] = 0;
 #pragma unroll
-                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = sm[(t1 + N1 * bin_to_tern(b2)) * 32 + lane];
+                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * 32 + lane];
                     cube_merge<R2>(v);
                     cube_reduce<R2>(v);
 #pragma unroll
-                    for (int x = 0; x < N2; x++) sm[(t1 + N1 * x) * 32 + lane] = v[x];
+                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
                 }
                 bar_compute(NCT);
                 // round 3: reduce the R1 axes
-                for (int t2 = warp; t2 < N2; t2 += kComputeWarps) {
+                for (int t2 = warp; t2 < N2; t2 += CW) {
                     uint32_t v[N1];
 #pragma unroll
-                    for (int x = 0; x < N1; x++) v[x] = sm[(x + N1 * t2) * 32 + lane];
+                    for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
                     cube_reduce<R1>(v);
 #pragma unroll
-                    for (int x = 0; x < N1; x++) sm[(x + N1 * t2) * 32 + lane] = v[x];
+                    for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
                 }
             }
         } else {
             // round 1: reduce the R1 axes
-            for (int t2 = warp; t2 < N2; t2 += kComputeWarps) {
+            for (int t2 = warp; t2 < N2; t2 += CW) {
                 uint32_t v[N1];
 #pragma unroll
-                for (int x = 0; x < N1; x++) v[x] = sm[(x + N1 * t2) * 32 + lane];
+                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
                 cube_reduce<R1>(v);
 #pragma unroll
-                for (int x = 0; x < N1; x++) sm[(x + N1 * t2) * 32 + lane] = v[x];
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
             }
             if (R2 > 0) {
                 bar_compute(NCT);
-                for (int t1 = warp; t1 < N1; t1 += kComputeWarps) {
+                for (int t1 = warp; t1 < N1; t1 += CW) {
                     uint32_t v[N2];
 #pragma unroll
-                    for (int x = 0; x < N2; x++) v[x] = sm[(t1 + N1 * x) * 32 + lane];
+                    for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * 32 + lane];
                     cube_reduce<R2>(v);
 #pragma unroll
-                    for (int x = 0; x < N2; x++) sm[(t1 + N1 * x) * 32 + lane] = v[x];
+                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
                 }
             }
         }
         if (ib_mask) {
             bar_compute(NCT);
+            // in-block axes, thread per block; halves swapped on lanes 4-7 of
+            // every 8 so each LDS.128/STS.128 quarter-warp hits 32 distinct banks
+            const int h = (lane >> 2) & 1;
             for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
-                uint4 *p = reinterpret_cast<uint4 *>(sm + t * 8);
-                const uint4 x0 = p[0], x1 = p[1];
+                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
                 inblock_reduce(v, ib_mask);
-                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
+                p[h] = h ? z1 : z0;
+                p[h ^ 1] = h ? z0 : z1;
             }
         }
         fence_async_smem();
@@ -837,21 +861,21 @@ Plan make_plan(int n) {
         }
     }
     // distribute the five in-block REDUCE axes over the passes that hold whole
-    // blocks (pass C: 1, each pass D: 2, pass E: 1; leftovers alternate C/E)
+    // blocks: pass C (write-only) takes 1, the read+write passes D share the
+    // rest (their HBM time leaves the most ALU slack), the final pass E takes
+    // none when a D pass exists (it is issue-bound by the C0 axes + compaction).
     if (p.T == 0) {
         p.ib_E = 31u;
+    } else if (p.m == 1) {
+        p.ib_C = 3u;   // axes 1,2
+        p.ib_E = 28u;  // axes 3,4,5
     } else {
-        int axis = 0;
-        auto take = [&](uint32_t &mask, int cnt) {
-            for (int c = 0; c < cnt && axis < 5; c++) mask |= 1u << axis++;
-        };
-        take(p.ib_C, 1);
-        for (int k = p.m - 2; k >= 0; k--) take(p.ib_D[k], 2);
-        take(p.ib_E, 1);
-        bool toC = false;
-        while (axis < 5) {
-            take(toC ? p.ib_C : p.ib_E, 1);
-            toC = !toC;
+        p.ib_C = 1u;
+        int axis = 1;
+        const int nd = p.m - 1;
+        for (int q = 0; q < nd; q++) {
+            const int take = (4 - (axis - 1)) / (nd - q);
+            for (int c = 0; c < take; c++) p.ib_D[p.m - 2 - q] |= 1u << axis++;
         }
     }
     return p;
@@ -951,8 +975,7 @@ int set_strided_attr() {
 template <int R1, int R2, int MODE>
 int set_pipe_attr() {
     using SM = PipeSmem<R1, R2>;
-    constexpr int smem = (2 * SM::TILE_WORDS + 2 * SM::STAGE_WORDS) * 4;
-    CK(cudaFuncSetAttribute(k_strided_pipe<R1, R2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_strided_pipe<R1, R2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::SMEM));
     return DQMC_OK;
 }
 
@@ -1059,16 +1082,55 @@ int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t
     return DQMC_OK;
 }
 
+// 5-D map for the binary-row gather of a MERGE_REDUCE group: dims {8Q words,
+// 3 x R1 digit dims (strides Q, 3Q, 9Q blocks), 3^R2}; box {32, 2, .., 2, 1}.
+int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2) {
+    cuuint64_t dims[5];
+    cuuint64_t strides[4];
+    cuuint32_t box[5], es[5];
+    int rank = 0;
+    dims[rank] = (cuuint64_t)(8 * Q);
+    box[rank] = 32;
+    es[rank++] = 1;
+    int64_t st = Q * 32;
+    for (int k = 0; k < r1; k++) {
+        dims[rank] = 3;
+        strides[rank - 1] = (cuuint64_t)st;
+        box[rank] = 2;
+        es[rank++] = 1;
+        st *= 3;
+    }
+    while (rank < 4) {  // pad to a fixed 5-D layout with unit dims
+        dims[rank] = 1;
+        strides[rank - 1] = (cuuint64_t)st;
+        box[rank] = 1;
+        es[rank++] = 1;
+    }
+    dims[rank] = (cuuint64_t)pow3l(r2);
+    strides[rank - 1] = (cuuint64_t)st;
+    box[rank] = 1;
+    es[rank++] = 1;
+    CUresult r = g_eng.encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, state, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed: " + std::to_string((int)r));
+    return DQMC_OK;
+}
+
 template <int R1, int R2, int MODE>
 int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
     using SM = PipeSmem<R1, R2>;
-    CUtensorMap map;
+    CUtensorMap map, gmap;
     int rc;
     if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR))) return rc;
+    if (MODE == MERGE_REDUCE) {
+        if ((rc = make_gather_map(&gmap, state, Q, R1, R2))) return rc;
+    } else {
+        gmap = map;
+    }
     const int64_t nitems = ncol * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
-    constexpr int smem = (2 * SM::TILE_WORDS + 2 * SM::STAGE_WORDS) * 4;
-    k_strided_pipe<R1, R2, MODE><<<grid, kPipeThreads, smem, s>>>(map, state, Q, ncol, nitems, ib);
+    k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
     CK(cudaGetLastError());
     return DQMC_OK;
 }
