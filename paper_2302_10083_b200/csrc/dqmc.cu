@@ -167,19 +167,16 @@ __device__ void tile_reduce_c0(uint32_t *sm, int g) {
 }
 
 struct FinalArgs {
-    int64_t *ranks;            // may be null (count only)
-    int64_t cap;               // capacity of ranks
-    int64_t rank_sub;          // subtracted from every rank (dummy-variable padding)
-    uint32_t ib_mask;          // in-block axes reduced in this pass
-    uint32_t *bitmap_out;      // write final bitmap here (null: do not)
-    unsigned long long *flags; // look-back descriptors, one per tile
-    int64_t *total;            // written by the last tile
-    int64_t ntiles;
+    int64_t *out;               // scratch (multi-tile) or final ranks (single tile); null = count only
+    int64_t cap;                // capacity of out
+    int64_t rank_sub;           // subtracted from every rank (dummy-variable padding)
+    uint32_t ib_mask;           // in-block axes reduced in this pass
+    uint32_t *bitmap_out;       // write final bitmap here (null: do not)
+    unsigned long long *alloc;  // running scratch allocation counter
+    int64_t *tile_base;         // per tile: offset of its ranks in out
+    int32_t *tile_cnt;          // per tile: prime count
 };
 
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagInc = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 // In-block reduce, popcount, decoupled look-back and ordered compaction of one
 // tile (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order
@@ -234,53 +231,25 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     if (lane == 0) s_warp_off[warp] = wsum;
     __syncthreads();
 
-    // (2) tile prefix: exclusive scan over warps + decoupled look-back done by
-    //     warp 0, 32 predecessors per step (one flag word each: status|value)
-    if (warp == 0) {
-        int64_t agg = 0;
-        if (lane == 0) {
-            int64_t acc = 0;
-            for (int w = 0; w < nwarps; w++) {
-                const int64_t c = s_warp_off[w];
-                s_warp_off[w] = acc;
-                acc += c;
-            }
-            agg = acc;
+    // (2) reserve this tile's range in the scratch output with one atomic (no
+    //     waiting on other tiles); k_scan_tiles + k_reorder restore rank order.
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int w = 0; w < nwarps; w++) {
+            const int64_t c = s_warp_off[w];
+            s_warp_off[w] = acc;
+            acc += c;
         }
-        agg = __shfl_sync(0xffffffffu, agg, 0);
-        volatile unsigned long long *flags = fa.flags;
-        int64_t excl = 0;
-        if (tile == 0) {
-            if (lane == 0) flags[0] = kFlagInc | (unsigned long long)agg;
-        } else {
-            if (lane == 0) flags[tile] = kFlagAgg | (unsigned long long)agg;
-            int64_t p = tile - 1;
-            while (true) {
-                const int64_t q = p - lane;
-                const unsigned long long f = q >= 0 ? flags[q] : (2ull << 62);
-                const unsigned long long st = f & ~kValMask;
-                if (__any_sync(0xffffffffu, st == 0)) continue;  // a predecessor is still counting
-                const unsigned incm = __ballot_sync(0xffffffffu, st == kFlagInc);
-                const int first = incm ? __ffs(incm) - 1 : 32;
-                int64_t v = lane <= first ? (int64_t)(f & kValMask) : 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                excl += v;
-                if (incm) break;
-                p -= 32;
-            }
-            if (lane == 0) flags[tile] = kFlagInc | (unsigned long long)(excl + agg);
-        }
-        if (lane == 0) {
-            if (tile == fa.ntiles - 1) *fa.total = excl + agg;
-            s_tile_off = excl;
-        }
+        const int64_t base = acc ? (int64_t)atomicAdd(fa.alloc, (unsigned long long)acc) : 0;
+        fa.tile_base[tile] = base;
+        fa.tile_cnt[tile] = (int32_t)acc;
+        s_tile_off = base;
     }
     __syncthreads();
-    if (fa.ranks == nullptr) return;
+    if (fa.out == nullptr) return;
 
-    // (3) ordered emission, lane = block: warp-inclusive scan of the block
-    //     counts kept from (1); only nonzero blocks are re-read.
+    // (3) ordered emission within the tile, lane = block: warp-inclusive scan
+    //     of the block counts kept from (1); only nonzero blocks are re-read.
     int64_t off = s_tile_off + s_warp_off[warp];
 #pragma unroll
     for (int j = 0; j < kMaxIter; j++) {
@@ -304,7 +273,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                         while (w) {
                             const int bit = __ffs(w) - 1;
                             w &= w - 1;
-                            if (pos < fa.cap) fa.ranks[pos] = base + k * 32 + bit;
+                            if (pos < fa.cap) fa.out[pos] = base + k * 32 + bit;
                             pos++;
                         }
                     }
@@ -312,6 +281,48 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                 off += __shfl_sync(0xffffffffu, incl, 31);
             }
         }
+    }
+}
+
+// Exclusive scan of the per-tile counts (one CTA) -> rank-order positions and
+// the total prime count.
+__global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__ cnt, int64_t *__restrict__ pos,
+                                                     int64_t n, int64_t *total) {
+    __shared__ int64_t s_part[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = min(n, t * per), hi = min(n, lo + per);
+    int64_t acc = 0;
+    for (int64_t i = lo; i < hi; i++) acc += cnt[i];
+    s_part[t] = acc;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int64_t y = t >= o ? s_part[t - o] : 0;
+        __syncthreads();
+        s_part[t] += y;
+        __syncthreads();
+    }
+    int64_t run = s_part[t] - acc;
+    for (int64_t i = lo; i < hi; i++) {
+        pos[i] = run;
+        run += cnt[i];
+    }
+    if (t == blockDim.x - 1) *total = s_part[t];
+}
+
+// Copy every tile's ranks from its scratch range to its rank-order position
+// (one warp per tile, coalesced 8-B copies).
+__global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
+                                                 const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
+                                                 int64_t *__restrict__ out, int64_t cap, int64_t ntiles) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t t = w; t < ntiles; t += nw) {
+        const int c = cnt[t];
+        const int64_t src = base[t], dst = pos[t];
+        for (int i = lane; i < c; i += 32)
+            if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
     }
 }
 
@@ -430,23 +441,18 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__res
 // pass E: one CTA per C0 tile (3^G blocks), tiles taken in rank order by
 // ticket; the tile arrives in shared memory with one TMA bulk copy.
 template <int G>
-__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, unsigned int *ticket,
-                                                           FinalArgs fa) {
+__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ __align__(8) uint64_t mbar;
-    __shared__ int64_t s_tile;
     constexpr int NB = pow3i(G);
-    if (threadIdx.x == 0) {
-        s_tile = atomicAdd(ticket, 1u);
-        mbar_init(&mbar, 1);
-    }
-    __syncthreads();
-    const int64_t tile = s_tile;
+    const int64_t tile = blockIdx.x;
     const int64_t blk0 = tile * NB;
     if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
         mbar_expect_tx(&mbar, NB * 32);
         bulk_g2s(sm, state + blk0 * 8, NB * 32, &mbar);
     }
+    __syncthreads();
     mbar_wait(&mbar, 0);
     tile_reduce_c0_t<G, 0>(sm);
     tile_finish(sm, NB, tile, blk0, fa);
@@ -905,9 +911,12 @@ struct Engine {
     cudaStream_t stream = nullptr;
     uint32_t *state = nullptr;
     size_t state_cap = 0;  // bytes
-    unsigned long long *flags = nullptr;
-    size_t flags_cap = 0;  // entries
-    unsigned int *ticket = nullptr;
+    int64_t *tile_base = nullptr, *tile_pos = nullptr;
+    int32_t *tile_cnt = nullptr;
+    size_t tile_cap = 0, tile_pos_cap = 0, tile_cnt_cap = 0;  // entries
+    int64_t *scratch = nullptr;
+    size_t scratch_cap = 0, scratch_want = 0;  // entries
+    unsigned long long *alloc = nullptr;
     int64_t *total = nullptr;
     uint32_t *tt_tmp = nullptr;
     size_t tt_tmp_cap = 0;  // bytes
@@ -939,7 +948,7 @@ int ensure_device() {
     CK(cudaSetDevice(dev));
     g_eng.device = dev;
     CK(cudaStreamCreateWithFlags(&g_eng.stream, cudaStreamNonBlocking));
-    CK(cudaMalloc(&g_eng.ticket, 256));
+    CK(cudaMalloc(&g_eng.alloc, 256));
     CK(cudaMalloc(&g_eng.total, 256));
     return DQMC_OK;
 }
@@ -1175,7 +1184,59 @@ uint64_t state_bytes_ref(int n, int h) {
 
 uint64_t engine_device_bytes(const Plan &p, bool keep) {
     if (p.T == 0 && !keep) return 0;
-    return (uint64_t)p.nblocks * 32 + (uint64_t)pow3l(p.T) * 8;
+    return (uint64_t)p.nblocks * 32 + (uint64_t)pow3l(p.T) * 20;
+}
+
+// Final stage: E (+ scan + reorder). Returns the total prime count.
+int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, bool count_only, bool keep,
+              int64_t *count, Timer &tm, cudaStream_t s) {
+    const uint64_t S = (uint64_t)p.nblocks * 32;
+    const int64_t ntiles = p.T == 0 ? 1 : pow3l(p.T);
+    const int tile_smem = (int)pow3l(p.g) * 32;
+    int rc;
+    if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    const bool direct = p.T == 0;  // one tile: its ranks are already in order
+    if (!count_only && !direct) {
+        const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+    }
+    FinalArgs fa;
+    fa.out = count_only ? nullptr : (direct ? ranks : g_eng.scratch);
+    fa.cap = count_only ? 0 : (direct ? cap : (int64_t)g_eng.scratch_cap);
+    fa.rank_sub = p.rank_sub;
+    fa.bitmap_out = keep ? g_eng.state : nullptr;
+    fa.alloc = g_eng.alloc;
+    fa.tile_base = g_eng.tile_base;
+    fa.tile_cnt = g_eng.tile_cnt;
+    CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
+    if (p.T == 0) {
+        fa.ib_mask = p.ib_E;
+        k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
+        CK(cudaGetLastError());
+        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (keep ? S : 0));
+    } else {
+        fa.ib_mask = p.ib_E;
+        k_c0_final<kC0Max><<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, fa);
+        CK(cudaGetLastError());
+        tm.mark("k_c0_final", S + (keep ? S : 0));
+    }
+    k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
+    CK(cudaGetLastError());
+    tm.mark("k_scan_tiles", (uint64_t)ntiles * 12);
+    if (!count_only && !direct) {
+        const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
+        k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos, ranks, cap,
+                                       ntiles);
+        CK(cudaGetLastError());
+        tm.mark("k_reorder", (uint64_t)ntiles * 16);
+    }
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *count = total;
+    return DQMC_OK;
 }
 
 // Run the whole plan on a device-resident 32-bit truth table.
@@ -1183,31 +1244,18 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
              cudaStream_t s) {
     Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
     const bool keep = (flags & DQMC_FLAG_KEEP_BITMAP) != 0;
+    const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0 || ranks == nullptr;
     int rc;
     const uint64_t S = (uint64_t)p.nblocks * 32;
     if (p.T > 0 || keep) {
         if ((rc = grow(g_eng.state, g_eng.state_cap, S, 1))) return rc;
     }
-    if ((rc = grow(g_eng.flags, g_eng.flags_cap, (size_t)std::max<int64_t>(1, pow3l(p.T)), 8))) return rc;
-    FinalArgs fa;
-    fa.ranks = (flags & DQMC_FLAG_COUNT_ONLY) ? nullptr : ranks;
-    fa.cap = fa.ranks ? cap : 0;
-    fa.rank_sub = p.rank_sub;
-    fa.flags = g_eng.flags;
-    fa.total = g_eng.total;
-    fa.bitmap_out = keep ? g_eng.state : nullptr;
     const int tile_smem = (int)pow3l(p.g) * 32;
     tm.begin();
-    if (p.T == 0) {
-        fa.ib_mask = p.ib_E;
-        fa.ntiles = 1;
-        k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
-        CK(cudaGetLastError());
-        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (keep ? S : 0));
-    } else {
+    if (p.T > 0) {
         // pass A
         const int64_t ntA = 1ll << p.T;
-        const int gridA = (int)std::min<int64_t>(ntA, 148ll * 8);
+        const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
         k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, g_eng.state, p.g, p.T);
         CK(cudaGetLastError());
         tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
@@ -1222,7 +1270,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
             const int64_t nitems = ncol << above;
             launch_strided_mode<MERGE_ONLY>(p.r[k], g_eng.state, Q, ncol, nitems, 0, s);
             CK(cudaGetLastError());
-            tm.mark("k_strided<MERGE_ONLY>", (uint64_t)(frac(above + p.r[k]) + (frac(above) - frac(above + p.r[k]))));
+            tm.mark("k_strided<MERGE_ONLY>", (uint64_t)frac(above));
         }
         // pass C: last group, merge + reduce
         {
@@ -1242,20 +1290,23 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
                 return rc;
             tm.mark("k_strided<REDUCE>", 2 * S);
         }
-        // pass E
-        const int64_t ntiles = pow3l(p.T);
-        CK(cudaMemsetAsync(g_eng.ticket, 0, sizeof(unsigned int), s));
-        CK(cudaMemsetAsync(g_eng.flags, 0, (size_t)ntiles * 8, s));
-        fa.ib_mask = p.ib_E;
-        fa.ntiles = ntiles;
-        k_c0_final<kC0Max><<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, g_eng.ticket, fa);
-        CK(cudaGetLastError());
-        tm.mark("k_c0_final", S + (keep ? S : 0));
     }
     int64_t total = 0;
-    CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (fa.ranks && !tm.bytes.empty()) tm.bytes.back() += (uint64_t)std::min<int64_t>(total, cap) * 8;
+    if ((rc = run_final(p, tt32, ranks, cap, count_only, keep, &total, tm, s))) return rc;
+    if (!count_only && p.T > 0 && (size_t)total > g_eng.scratch_cap) {
+        // the scratch was too small: only the final stage is rerun (it does not
+        // modify the merged state; with KEEP_BITMAP it rewrites the same P)
+        g_eng.scratch_want = (size_t)((double)total * 1.05) + 1024;
+        tm.on = false;
+        if ((rc = run_final(p, tt32, ranks, cap, count_only, keep, &total, tm, s))) return rc;
+    }
+    if (!count_only && !tm.bytes.empty()) {
+        const uint64_t written = (uint64_t)std::min<int64_t>(total, cap) * 8;
+        for (size_t i = 0; i < tm.names.size(); i++) {
+            if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += written;
+            if (tm.names[i] == "k_reorder") tm.bytes[i] += 2 * written;
+        }
+    }
     tm.finish();
     *count = total;
     g_eng.state_n = keep ? p.n : -1;
@@ -1550,8 +1601,11 @@ void dqmc_release(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_eng.device < 0) return;
     cudaFree(g_eng.state);
-    cudaFree(g_eng.flags);
-    cudaFree(g_eng.ticket);
+    cudaFree(g_eng.tile_base);
+    cudaFree(g_eng.tile_pos);
+    cudaFree(g_eng.tile_cnt);
+    cudaFree(g_eng.scratch);
+    cudaFree(g_eng.alloc);
     cudaFree(g_eng.total);
     cudaFree(g_eng.tt_tmp);
     cudaFree(g_eng.in_tmp);
