@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -314,13 +315,17 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__
 // (one warp per tile, coalesced 8-B copies).
 __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
                                                  const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
-                                                 int64_t *__restrict__ out, int64_t cap, int64_t ntiles) {
+                                                 int64_t *__restrict__ out, int64_t cap, int64_t ntiles,
+                                                 int64_t scap) {
     const int lane = threadIdx.x & 31;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
     for (int64_t t = w; t < ntiles; t += nw) {
         const int c = cnt[t];
         const int64_t src = base[t], dst = pos[t];
+        // a tile whose range overflowed the scratch is skipped: the host sees
+        // total > scratch capacity, grows the scratch and reruns the final stage
+        if (c < 0 || src < 0 || src + c > scap) continue;
         for (int i = lane; i < c; i += 32)
             if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
     }
@@ -888,6 +893,7 @@ Plan make_plan(int n) {
 }
 
 thread_local std::string g_err;
+const bool g_debug = getenv("DQMC_DEBUG") != nullptr;  // sync + report after every pass
 std::mutex g_mu;
 
 int set_err(int code, const std::string &msg) {
@@ -1036,6 +1042,13 @@ struct Timer {
     std::vector<std::string> names;
     std::vector<uint64_t> bytes;
     void mark(const char *name, uint64_t b) {
+        if (g_debug) {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) {
+                fprintf(stderr, "[dqmc debug] %s failed: %s\n", name, cudaGetErrorString(e));
+                fflush(stderr);
+            }
+        }
         if (!on) return;
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -1228,7 +1241,7 @@ int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, 
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
         k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos, ranks, cap,
-                                       ntiles);
+                                       ntiles, (int64_t)g_eng.scratch_cap);
         CK(cudaGetLastError());
         tm.mark("k_reorder", (uint64_t)ntiles * 16);
     }
