@@ -107,6 +107,23 @@ int dqmc_state_download(void *host, uint64_t bytes);
 /* Device-side synthetic inputs (frozen generator of ttio.py:331-378 and the
  * survey's 3-way / S-box variants); writes 2^n uint8. */
 int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint64_t seed, void *stream);
+/* Points [x0, x0 + count) only (a rank's slice of a sharded table). */
+int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, double p_on, double p_dc, uint64_t seed,
+                           void *stream);
+
+/* Building blocks of the sharded multi-GPU path, all on
+ * device buffers in the h = 5 layout (n >= 5):
+ * dqmc_merge_device: complete MERGE of all n dimensions (no REDUCE) into
+ *   state_out (dqmc_state_bytes(n, 5) bytes) — the implicant bitmap M of
+ *   the (sub-)function, DenseState.words after run_pass(MERGE) (dense.py:296-315).
+ * dqmc_reduce_extract_device: REDUCE of all n dimensions in place, then clear
+ *   the cells set in kill (may be NULL; the OR of the top-axis parent bitmaps),
+ *   then ordered compaction of the survivors as ranks + rank_offset.
+ * dqmc_bitop_device: dst = a & b (op 0) or a | b (op 1), nbytes % 16 == 0. */
+int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state_out, void *stream);
+int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int64_t rank_offset, int64_t *ranks_dev,
+                               int64_t ranks_cap, int64_t *count_out, uint32_t flags, void *stream);
+int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint64_t nbytes, int op, void *stream);
 
 /* The pass plan the engine runs for n variables (host logic, no GPU needed):
  * out = {ne, H, g, T, m, r[0..7], a[0..7], ib_C, ib_E, ib_D[0..7], rank_sub}

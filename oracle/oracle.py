@@ -123,6 +123,16 @@ class OracleState:
         self.words = np.zeros(state_bytes(n, self.h) // 8, dtype=np.uint64)
         lib().oracle_load(_words(tt_words, n).ctypes.data, n, self.h, self.words.ctypes.data)
 
+    @classmethod
+    def from_words(cls, words: np.ndarray, n: int, h: int = 5) -> "OracleState":
+        """Wrap an existing state array (uint64, DenseState.words layout)."""
+        st = cls.__new__(cls)
+        st.n, st.h = n, h
+        st.words = np.ascontiguousarray(words, dtype=np.uint64)
+        if st.words.shape != (state_bytes(n, h) // 8,):
+            raise ValueError("state size does not match n, h")
+        return st
+
     def run_pass(self, op: int, dims=None, optimized: bool = True) -> dict:
         if dims is None:
             dims = list(range(self.h + 1, self.n + 1)) + list(range(1, self.h + 1))

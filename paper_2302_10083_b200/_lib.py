@@ -49,6 +49,10 @@ EXPORTS = (
     "dqmc_state_device",
     "dqmc_state_download",
     "dqmc_gen3_device",
+    "dqmc_gen3_range_device",
+    "dqmc_merge_device",
+    "dqmc_reduce_extract_device",
+    "dqmc_bitop_device",
     "dqmc_plan",
     "dqmc_release",
 )
@@ -105,6 +109,10 @@ def load() -> ctypes.CDLL:
             "dqmc_state_device": (i32, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)]),
             "dqmc_state_download": (i32, [vp, u64]),
             "dqmc_gen3_device": (i32, [vp, i32, dbl, dbl, u64, vp]),
+            "dqmc_gen3_range_device": (i32, [vp, i64, i64, dbl, dbl, u64, vp]),
+            "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
+            "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),
+            "dqmc_bitop_device": (i32, [vp, vp, vp, u64, i32, vp]),
             "dqmc_plan": (i32, [i32, ctypes.POINTER(ctypes.c_int64), i32]),
             "dqmc_release": (None, []),
         }

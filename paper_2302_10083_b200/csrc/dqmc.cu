@@ -107,11 +107,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 
 // three-way generator: value of point x from the frozen
 // counter generator mix(seed + (x+1)*GAMMA) >> 11 (ttio.py:341-343, 365-374)
-__global__ void k_gen3(uint8_t *__restrict__ out, int64_t npts, uint64_t seed, uint64_t t_on, uint64_t t_any) {
+__global__ void k_gen3(uint8_t *__restrict__ out, int64_t x0, int64_t npts, uint64_t seed, uint64_t t_on,
+                       uint64_t t_any) {
     const int64_t stride = gridDim.x * (int64_t)blockDim.x;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < npts; x += stride) {
-        const uint64_t u = mix64(seed + (uint64_t)(x + 1) * 0x9E3779B97F4A7C15ull) >> 11;
-        out[x] = u < t_on ? 1 : (u < t_any ? 2 : 0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts; i += stride) {
+        const uint64_t x = (uint64_t)(x0 + i);
+        const uint64_t u = mix64(seed + (x + 1) * 0x9E3779B97F4A7C15ull) >> 11;
+        out[i] = u < t_on ? 1 : (u < t_any ? 2 : 0);
     }
 }
 
@@ -170,7 +172,8 @@ __device__ void tile_reduce_c0(uint32_t *sm, int g) {
 struct FinalArgs {
     int64_t *out;               // scratch (multi-tile) or final ranks (single tile); null = count only
     int64_t cap;                // capacity of out
-    int64_t rank_sub;           // subtracted from every rank (dummy-variable padding)
+    int64_t rank_add;           // added to every rank (dummy-variable padding < 0, top-block offset > 0)
+    const uint32_t *kill;       // optional: cells to clear after the low reduce (kills from top parents)
     uint32_t ib_mask;           // in-block axes reduced in this pass
     uint32_t *bitmap_out;       // write final bitmap here (null: do not)
     unsigned long long *alloc;  // running scratch allocation counter
@@ -212,6 +215,14 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                     inblock_reduce(v, fa.ib_mask);
                     x0 = make_uint4(v[0], v[1], v[2], v[3]);
                     x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                }
+                if (fa.kill) {
+                    const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill + (blk0 + b) * 8);
+                    const uint4 k0 = kq[0], k1 = kq[1];
+                    x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
+                    x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
+                }
+                if (fa.ib_mask || fa.kill) {
                     p[h] = h ? x1 : x0;
                     p[h ^ 1] = h ? x0 : x1;
                 }
@@ -266,7 +277,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                 if (c) {
                     int64_t pos = off + incl - c;
                     const int b = b0 + 32 * j + lane;
-                    const int64_t base = (blk0 + b) * 243 - fa.rank_sub;
+                    const int64_t base = (blk0 + b) * 243 + fa.rank_add;
                     const uint32_t *wp = sm + b * 8;
 #pragma unroll 1
                     for (int k = 0; k < 8; k++) {
@@ -328,6 +339,18 @@ __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scr
         if (c < 0 || src < 0 || src + c > scap) continue;
         for (int i = lane; i < c; i += 32)
             if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
+    }
+}
+
+// dst = a & b (op 0) or a | b (op 1), 16 B per thread: the top-axis block
+// ANDs of the sharded path (M_t = AND over completions) and kill accumulation.
+__global__ void k_bitop(uint4 *__restrict__ dst, const uint4 *__restrict__ a, const uint4 *__restrict__ b, int64_t n16,
+                        int op) {
+    const int64_t stride = gridDim.x * (int64_t)blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride) {
+        const uint4 x = __ldcs(a + i), y = __ldcs(b + i);
+        dst[i] = op == 0 ? make_uint4(x.x & y.x, x.y & y.y, x.z & y.z, x.w & y.w)
+                         : make_uint4(x.x | y.x, x.y | y.y, x.z | y.z, x.w | y.w);
     }
 }
 
@@ -1200,9 +1223,26 @@ uint64_t engine_device_bytes(const Plan &p, bool keep) {
     return (uint64_t)p.nblocks * 32 + (uint64_t)pow3l(p.T) * 20;
 }
 
-// Final stage: E (+ scan + reorder). Returns the total prime count.
-int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, bool count_only, bool keep,
-              int64_t *count, Timer &tm, cudaStream_t s) {
+int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArgs &fa, cudaStream_t s) {
+    const int smem = (int)pow3l(g) * 32;
+    switch (g) {
+#define CASE(G)                                                                         \
+    case G:                                                                             \
+        k_c0_final<G><<<(unsigned)ntiles, kTileThreads, smem, s>>>(state, fa);          \
+        break;
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+        default: return set_err(DQMC_ERR_INVALID, "bad tile exponent");
+    }
+    CK(cudaGetLastError());
+    return DQMC_OK;
+}
+
+// Final stage: E (+ scan + reorder). Source: the truth table (k_small, fused
+// A+E, when tt32 != null) or a merged/reduced state. Returns the prime count.
+int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const uint32_t *kill, uint32_t ib_mask,
+              int64_t rank_add, int64_t *ranks, int64_t cap, bool count_only, uint32_t *bitmap_out, int64_t *count,
+              Timer &tm, cudaStream_t s) {
     const uint64_t S = (uint64_t)p.nblocks * 32;
     const int64_t ntiles = p.T == 0 ? 1 : pow3l(p.T);
     const int tile_smem = (int)pow3l(p.g) * 32;
@@ -1210,7 +1250,7 @@ int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, 
     if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
-    const bool direct = p.T == 0;  // one tile: its ranks are already in order
+    const bool direct = ntiles == 1;  // one tile: its ranks are already in order
     if (!count_only && !direct) {
         const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
         if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
@@ -1218,22 +1258,21 @@ int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, 
     FinalArgs fa;
     fa.out = count_only ? nullptr : (direct ? ranks : g_eng.scratch);
     fa.cap = count_only ? 0 : (direct ? cap : (int64_t)g_eng.scratch_cap);
-    fa.rank_sub = p.rank_sub;
-    fa.bitmap_out = keep ? g_eng.state : nullptr;
+    fa.rank_add = rank_add;
+    fa.kill = kill;
+    fa.ib_mask = ib_mask;
+    fa.bitmap_out = bitmap_out;
     fa.alloc = g_eng.alloc;
     fa.tile_base = g_eng.tile_base;
     fa.tile_cnt = g_eng.tile_cnt;
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
-    if (p.T == 0) {
-        fa.ib_mask = p.ib_E;
+    if (tt32) {
         k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
         CK(cudaGetLastError());
-        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (keep ? S : 0));
+        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (bitmap_out ? S : 0));
     } else {
-        fa.ib_mask = p.ib_E;
-        k_c0_final<kC0Max><<<(unsigned)ntiles, kTileThreads, tile_smem, s>>>(g_eng.state, fa);
-        CK(cudaGetLastError());
-        tm.mark("k_c0_final", S + (keep ? S : 0));
+        if ((rc = launch_c0_final(p.g, ntiles, state, fa, s))) return rc;
+        tm.mark("k_c0_final", S + (kill ? S : 0) + (bitmap_out ? S : 0));
     }
     k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
     CK(cudaGetLastError());
@@ -1252,7 +1291,92 @@ int run_final(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, 
     return DQMC_OK;
 }
 
-// Run the whole plan on a device-resident 32-bit truth table.
+// MERGE passes. full = true: every group merge-only (the complete implicant
+// bitmap M is left in `state`, used by the sharded path); otherwise the last
+// group is left for the fused MERGE_REDUCE pass.
+int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, Timer &tm, cudaStream_t s) {
+    const uint64_t S = (uint64_t)p.nblocks * 32;
+    const int tile_smem = (int)pow3l(p.g) * 32;
+    const int64_t ntA = 1ll << p.T;
+    const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
+    k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T);
+    CK(cudaGetLastError());
+    tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
+    auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
+    const int last = full ? p.m : p.m - 1;
+    for (int k = 0; k < last; k++) {
+        const int64_t Q = pow3l(p.a[k]);
+        const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+        int above = 0;
+        for (int j = k + 1; j < p.m; j++) above += p.r[j];
+        const int64_t nitems = ncol << above;
+        launch_strided_mode<MERGE_ONLY>(p.r[k], state, Q, ncol, nitems, 0, s);
+        CK(cudaGetLastError());
+        tm.mark("k_strided<MERGE_ONLY>", (uint64_t)frac(above));
+    }
+    return DQMC_OK;
+}
+
+// REDUCE passes of the strided groups. fused: the last group is merged and
+// reduced in one pass (single-GPU plan); otherwise every group is reduce-only
+// (sharded path, M already complete). The in-block axes of pass C go with the
+// last group either way.
+int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s) {
+    const uint64_t S = (uint64_t)p.nblocks * 32;
+    int rc;
+    {
+        const int k = p.m - 1;
+        const int64_t Q = pow3l(p.a[k]);
+        const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+        if (fused) {
+            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
+            tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(S * std::pow(2.0 / 3.0, p.r[k]) + S));
+        } else {
+            if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
+            tm.mark("k_strided<REDUCE>", 2 * S);
+        }
+    }
+    for (int k = p.m - 2; k >= 0; k--) {
+        const int64_t Q = pow3l(p.a[k]);
+        const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
+        int above = 0;
+        for (int j = k + 1; j < p.m; j++) above += p.r[j];
+        if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above), p.ib_D[k], s))) return rc;
+        tm.mark("k_strided<REDUCE>", 2 * S);
+    }
+    return DQMC_OK;
+}
+
+void add_rank_bytes(Timer &tm, int64_t written) {
+    if (tm.bytes.empty()) return;
+    for (size_t i = 0; i < tm.names.size(); i++) {
+        if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += (uint64_t)written * 8;
+        if (tm.names[i] == "k_reorder") tm.bytes[i] += (uint64_t)written * 16;
+    }
+}
+
+// Final stage with the scratch-regrow retry (the stage does not modify the
+// merged state it reads; with a bitmap output it rewrites the same P).
+int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, const uint32_t *kill,
+                    uint32_t ib_mask, int64_t rank_add, int64_t *ranks, int64_t cap, bool count_only,
+                    uint32_t *bitmap_out, int64_t *count, Timer &tm, cudaStream_t s) {
+    int rc;
+    if ((rc = run_final(p, tt32, state, kill, ib_mask, rank_add, ranks, cap, count_only, bitmap_out, count, tm, s)))
+        return rc;
+    const bool direct = (p.T == 0);
+    if (!count_only && !direct && (size_t)*count > g_eng.scratch_cap) {
+        g_eng.scratch_want = (size_t)((double)*count * 1.05) + 1024;
+        const bool on = tm.on;
+        tm.on = false;
+        rc = run_final(p, tt32, state, kill, ib_mask, rank_add, ranks, cap, count_only, bitmap_out, count, tm, s);
+        tm.on = on;
+        if (rc) return rc;
+    }
+    if (!count_only) add_rank_bytes(tm, std::min<int64_t>(*count, cap));
+    return DQMC_OK;
+}
+
+// Run the whole single-GPU plan on a device-resident 32-bit truth table.
 int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, int64_t *count, uint32_t flags,
              cudaStream_t s) {
     Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
@@ -1263,62 +1387,18 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
     if (p.T > 0 || keep) {
         if ((rc = grow(g_eng.state, g_eng.state_cap, S, 1))) return rc;
     }
-    const int tile_smem = (int)pow3l(p.g) * 32;
     tm.begin();
-    if (p.T > 0) {
-        // pass A
-        const int64_t ntA = 1ll << p.T;
-        const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
-        k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, g_eng.state, p.g, p.T);
-        CK(cudaGetLastError());
-        tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
-        // fraction helper: (2/3)^k of S
-        auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
-        // passes B: merge-only groups 0..m-2 (outer digits of higher groups binary)
-        for (int k = 0; k + 1 < p.m; k++) {
-            const int64_t Q = pow3l(p.a[k]);
-            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
-            int above = 0;
-            for (int j = k + 1; j < p.m; j++) above += p.r[j];
-            const int64_t nitems = ncol << above;
-            launch_strided_mode<MERGE_ONLY>(p.r[k], g_eng.state, Q, ncol, nitems, 0, s);
-            CK(cudaGetLastError());
-            tm.mark("k_strided<MERGE_ONLY>", (uint64_t)frac(above));
-        }
-        // pass C: last group, merge + reduce
-        {
-            const int k = p.m - 1;
-            const int64_t Q = pow3l(p.a[k]);
-            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
-            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], g_eng.state, Q, ncol, 1, p.ib_C, s))) return rc;
-            tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(frac(p.r[k]) + S));
-        }
-        // passes D: reduce the other groups
-        for (int k = p.m - 2; k >= 0; k--) {
-            const int64_t Q = pow3l(p.a[k]);
-            const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
-            int above = 0;
-            for (int j = k + 1; j < p.m; j++) above += p.r[j];
-            if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], g_eng.state, Q, ncol, pow3l(above), p.ib_D[k], s)))
-                return rc;
-            tm.mark("k_strided<REDUCE>", 2 * S);
-        }
-    }
     int64_t total = 0;
-    if ((rc = run_final(p, tt32, ranks, cap, count_only, keep, &total, tm, s))) return rc;
-    if (!count_only && p.T > 0 && (size_t)total > g_eng.scratch_cap) {
-        // the scratch was too small: only the final stage is rerun (it does not
-        // modify the merged state; with KEEP_BITMAP it rewrites the same P)
-        g_eng.scratch_want = (size_t)((double)total * 1.05) + 1024;
-        tm.on = false;
-        if ((rc = run_final(p, tt32, ranks, cap, count_only, keep, &total, tm, s))) return rc;
-    }
-    if (!count_only && !tm.bytes.empty()) {
-        const uint64_t written = (uint64_t)std::min<int64_t>(total, cap) * 8;
-        for (size_t i = 0; i < tm.names.size(); i++) {
-            if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += written;
-            if (tm.names[i] == "k_reorder") tm.bytes[i] += 2 * written;
-        }
+    if (p.T > 0) {
+        if ((rc = run_merge(p, tt32, g_eng.state, false, tm, s))) return rc;
+        if ((rc = run_reduce(p, g_eng.state, true, tm, s))) return rc;
+        if ((rc = run_final_retry(p, nullptr, g_eng.state, nullptr, p.ib_E, -p.rank_sub, ranks, cap, count_only,
+                                  keep ? g_eng.state : nullptr, &total, tm, s)))
+            return rc;
+    } else {
+        if ((rc = run_final_retry(p, tt32, nullptr, nullptr, p.ib_E, -p.rank_sub, ranks, cap, count_only,
+                                  keep ? g_eng.state : nullptr, &total, tm, s)))
+            return rc;
     }
     tm.finish();
     *count = total;
@@ -1326,27 +1406,34 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
     return DQMC_OK;
 }
 
-// total device pass (input conversion + plan) with growable rank buffer
-int primes_device_impl(const void *in, int kind, int n, int64_t *ranks, int64_t cap, int64_t *count,
-                       uint32_t flags, cudaStream_t s) {
-    const Plan p = make_plan(n);
-    const uint32_t *tt32 = nullptr;
+// input conversion to 32-bit truth-table words for n >= 5 (or the padded word)
+int input_words(const void *in, int kind, int n, const uint32_t **tt32, cudaStream_t s) {
     int rc;
     if (n < 5) {
         if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, 256, 1))) return rc;
         k_pad_small<<<1, 32, 0, s>>>(in, kind, n, g_eng.tt_tmp);
         CK(cudaGetLastError());
-        tt32 = g_eng.tt_tmp;
+        *tt32 = g_eng.tt_tmp;
     } else if (kind == DQMC_IN_U8) {
         const int64_t nw = 1ll << (n - 5);
         if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, (size_t)nw * 4, 1))) return rc;
         const int grid = (int)std::min<int64_t>((nw * 32 + 255) / 256, 148ll * 32);
         k_u8_to_words<<<grid, 256, 0, s>>>((const uint8_t *)in, g_eng.tt_tmp, nw);
         CK(cudaGetLastError());
-        tt32 = g_eng.tt_tmp;
+        *tt32 = g_eng.tt_tmp;
     } else {
-        tt32 = (const uint32_t *)in;  // LE uint64 words viewed as uint32 words
+        *tt32 = (const uint32_t *)in;  // LE uint64 words viewed as uint32 words
     }
+    return DQMC_OK;
+}
+
+// total device pass (input conversion + plan)
+int primes_device_impl(const void *in, int kind, int n, int64_t *ranks, int64_t cap, int64_t *count,
+                       uint32_t flags, cudaStream_t s) {
+    const Plan p = make_plan(n);
+    const uint32_t *tt32 = nullptr;
+    int rc;
+    if ((rc = input_words(in, kind, n, &tt32, s))) return rc;
     return run_plan(p, tt32, ranks, cap, count, flags, s);
 }
 
@@ -1572,20 +1659,80 @@ int dqmc_state_download(void *host, uint64_t bytes) {
     return DQMC_OK;
 }
 
-int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint64_t seed, void *stream) {
+int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, double p_on, double p_dc, uint64_t seed,
+                           void *stream) {
     int rc;
-    if ((rc = validate(n, 0))) return rc;
+    if (!values_dev || x0 < 0 || count < 0) return set_err(DQMC_ERR_INVALID, "bad generator range");
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
     // int(p * 2^53) as Python computes it (float64 product, truncation)
     const uint64_t t_on = (uint64_t)(p_on * 9007199254740992.0);
     const uint64_t t_any = (uint64_t)((p_on + p_dc) * 9007199254740992.0);
-    const int64_t npts = 1ll << n;
-    const int grid = (int)std::min<int64_t>((npts + 255) / 256, 148ll * 64);
-    k_gen3<<<grid, 256, 0, s>>>(values_dev, npts, seed, t_on, t_any);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148ll * 64));
+    if (count) k_gen3<<<grid, 256, 0, s>>>(values_dev, x0, count, seed, t_on, t_any);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
+    return DQMC_OK;
+}
+
+int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint64_t seed, void *stream) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    return dqmc_gen3_range_device(values_dev, 0, 1ll << n, p_on, p_dc, seed, stream);
+}
+
+int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state_out, void *stream) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (n < 5) return set_err(DQMC_ERR_INVALID, "dqmc_merge_device needs n >= 5 (h=5 layout)");
+    if (!input_dev || !state_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    const Plan p = make_plan(n);
+    const uint32_t *tt32 = nullptr;
+    if ((rc = input_words(input_dev, in_kind, n, &tt32, s))) return rc;
+    Timer tm{false, s};
+    if ((rc = run_merge(p, tt32, state_out, true, tm, s))) return rc;
+    CK(cudaStreamSynchronize(s));
+    return DQMC_OK;
+}
+
+int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int64_t rank_offset, int64_t *ranks_dev,
+                               int64_t ranks_cap, int64_t *count_out, uint32_t flags, void *stream) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (n < 5) return set_err(DQMC_ERR_INVALID, "dqmc_reduce_extract_device needs n >= 5 (h=5 layout)");
+    if (!state || !count_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    if ((rc = ensure_attrs())) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    const Plan p = make_plan(n);
+    const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0 || ranks_dev == nullptr;
+    Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
+    tm.begin();
+    if (p.T > 0 && (rc = run_reduce(p, state, false, tm, s))) return rc;
+    if ((rc = run_final_retry(p, nullptr, state, kill, p.ib_E, rank_offset, ranks_dev, ranks_cap, count_only,
+                              (flags & DQMC_FLAG_KEEP_BITMAP) ? state : nullptr, count_out, tm, s)))
+        return rc;
+    tm.finish();
+    return DQMC_OK;
+}
+
+int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint64_t nbytes, int op, void *stream) {
+    int rc;
+    if (!dst || !a || !b || (nbytes % 16) || (op != 0 && op != 1))
+        return set_err(DQMC_ERR_INVALID, "bitop: null pointer, size not a multiple of 16, or bad op");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    const int64_t n16 = (int64_t)(nbytes / 16);
+    const int grid = (int)std::min<int64_t>((n16 + 255) / 256, 148ll * 16);
+    if (n16) k_bitop<<<grid, 256, 0, s>>>((uint4 *)dst, (const uint4 *)a, (const uint4 *)b, n16, op);
+    CK(cudaGetLastError());
     return DQMC_OK;
 }
 
