@@ -152,7 +152,7 @@ __device__ void tile_reduce_axes(uint32_t *sm, int g, int j0) {
         uint32_t v[N];
 #pragma unroll
         for (int i = 0; i < N; i++) v[i] = sm[(blk + i * sj) * 8 + w];
-        cube_reduce<K>(v);
+        cube_reduce_par<K>(v);
 #pragma unroll
         for (int i = 0; i < N; i++) sm[(blk + i * sj) * 8 + w] = v[i];
     }
@@ -260,8 +260,11 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     __syncthreads();
     if (fa.out == nullptr) return;
 
-    // (3) ordered emission within the tile, lane = block: warp-inclusive scan
-    //     of the block counts kept from (1); only nonzero blocks are re-read.
+    // (3) ordered emission within the tile. Per 32-block group: warp scan of
+    //     the block counts from (1), then a load-balanced walk: lane q of each
+    //     step finds the block holding output q (binary search over the scan
+    //     by shuffles) and that block's (q - excl)-th set bit, so every warp
+    //     store writes 32 consecutive ranks.
     int64_t off = s_tile_off + s_warp_off[warp];
 #pragma unroll
     for (int j = 0; j < kMaxIter; j++) {
@@ -274,23 +277,36 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                     const int y = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += y;
                 }
-                if (c) {
-                    int64_t pos = off + incl - c;
-                    const int b = b0 + 32 * j + lane;
-                    const int64_t base = (blk0 + b) * 243 + fa.rank_add;
-                    const uint32_t *wp = sm + b * 8;
-#pragma unroll 1
-                    for (int k = 0; k < 8; k++) {
-                        uint32_t w = wp[k];
-                        while (w) {
-                            const int bit = __ffs(w) - 1;
-                            w &= w - 1;
-                            if (pos < fa.cap) fa.out[pos] = base + k * 32 + bit;
-                            pos++;
+                const int excl = incl - c;
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                const int gb = b0 + 32 * j;  // first block of the group
+                for (int q0 = 0; q0 < total; q0 += 32) {
+                    const int q = q0 + lane;
+                    int L = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int ex = __shfl_sync(0xffffffffu, excl, L + step);
+                        if (ex <= q) L += step;
+                    }
+                    const int exL = __shfl_sync(0xffffffffu, excl, L);
+                    if (q < total) {
+                        int r = q - exL;
+                        const int blk = gb + L;
+                        const uint32_t *wp = sm + blk * 8;
+                        int k = 0;
+                        uint32_t w = wp[0];
+                        int pc = __popc(w);
+                        while (r >= pc) {
+                            r -= pc;
+                            w = wp[++k];
+                            pc = __popc(w);
                         }
+                        for (int t = 0; t < r; t++) w &= w - 1;
+                        const int64_t pos = off + q;
+                        if (pos < fa.cap) fa.out[pos] = (blk0 + blk) * 243 + k * 32 + (__ffs(w) - 1) + fa.rank_add;
                     }
                 }
-                off += __shfl_sync(0xffffffffu, incl, 31);
+                off += total;
             }
         }
     }
@@ -407,7 +423,7 @@ __device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
         uint32_t v[N];
 #pragma unroll
         for (int i = 0; i < N; i++) v[i] = sm[(blk + i * SJ) * 8 + w];
-        cube_reduce<K>(v);
+        cube_reduce_par<K>(v);
 #pragma unroll
         for (int i = 0; i < N; i++) sm[(blk + i * SJ) * 8 + w] = v[i];
     }
@@ -534,7 +550,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                 }
                 cube_merge<R1>(v);
                 if (MODE == MERGE_REDUCE && R2 == 0) {
-                    cube_reduce<R1>(v);
+                    cube_reduce_par<R1>(v);
 #pragma unroll
                     for (int i = 0; i < N1; i++) {
                         if (ib)
@@ -568,7 +584,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                         for (int i = 0; i < N2; i++)
                             if (has_star(i, R2) && act) g0[(int64_t)(t1 + N1 * i) * Qw] = v[i];
                     } else {
-                        cube_reduce<R2>(v);
+                        cube_reduce_par<R2>(v);
                         __syncwarp();
 #pragma unroll
                         for (int i = 0; i < N2; i++) sm[(t1 + N1 * i) * 32 + lane] = v[i];
@@ -581,7 +597,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                         uint32_t v[N1];
 #pragma unroll
                         for (int i = 0; i < N1; i++) v[i] = sm[(i + N1 * t2) * 32 + lane];
-                        cube_reduce<R1>(v);
+                        cube_reduce_par<R1>(v);
 #pragma unroll
                         for (int i = 0; i < N1; i++) {
                             if (ib)
@@ -599,7 +615,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                 uint32_t v[N1];
 #pragma unroll
                 for (int i = 0; i < N1; i++) v[i] = act ? __ldcs(g0 + (int64_t)(i + N1 * t2) * Qw) : 0u;
-                cube_reduce<R1>(v);
+                cube_reduce_par<R1>(v);
 #pragma unroll
                 for (int i = 0; i < N1; i++) {
                     if (R2 > 0 || ib)
@@ -614,7 +630,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                     uint32_t v[N2];
 #pragma unroll
                     for (int i = 0; i < N2; i++) v[i] = sm[(t1 + N1 * i) * 32 + lane];
-                    cube_reduce<R2>(v);
+                    cube_reduce_par<R2>(v);
                     __syncwarp();
 #pragma unroll
                     for (int i = 0; i < N2; i++) {
@@ -790,7 +806,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 #pragma unroll
                 for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * 32 + lane];
                 cube_merge<R1>(v);
-                if (R2 == 0) cube_reduce<R1>(v);
+                if (R2 == 0) cube_reduce_par<R1>(v);
 #pragma unroll
                 for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * 32 + lane] = v[x];
             }
@@ -804,7 +820,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 #pragma unroll
                     for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * 32 + lane];
                     cube_merge<R2>(v);
-                    cube_reduce<R2>(v);
+                    cube_reduce_par<R2>(v);
 #pragma unroll
                     for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
                 }
@@ -814,7 +830,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                     uint32_t v[N1];
 #pragma unroll
                     for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
-                    cube_reduce<R1>(v);
+                    cube_reduce_par<R1>(v);
 #pragma unroll
                     for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
                 }
@@ -825,7 +841,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 uint32_t v[N1];
 #pragma unroll
                 for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
-                cube_reduce<R1>(v);
+                cube_reduce_par<R1>(v);
 #pragma unroll
                 for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
             }
@@ -835,7 +851,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                     uint32_t v[N2];
 #pragma unroll
                     for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * 32 + lane];
-                    cube_reduce<R2>(v);
+                    cube_reduce_par<R2>(v);
 #pragma unroll
                     for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
                 }

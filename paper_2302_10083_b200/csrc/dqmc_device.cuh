@@ -64,6 +64,42 @@ __device__ __forceinline__ void cube_reduce(uint32_t (&v)[P3<K>::v]) {
     }
 }
 
+// number of fixed (0/1) digits among the K digits of idx
+__host__ __device__ constexpr int fixed_digits(int idx, int K) {
+    int f = 0;
+    for (int i = 0; i < K; i++) {
+        if (idx % 3 != 2) f++;
+        idx /= 3;
+    }
+    return f;
+}
+
+// REDUCE of all K axes as ONE parallel step (every kill read from the state
+// at step start): P(c) = M(c) & ~OR_{fixed axes i} M(c[i->*]). Done in place
+// by visiting cells from most fixed digits to fewest, so every parent (one
+// more star) is read before it is itself reduced. ~40% fewer LOP3 than the
+// axis-by-axis form; exact by the parallel-step argument.
+template <int K>
+__device__ __forceinline__ void cube_reduce_par(uint32_t (&v)[P3<K>::v]) {
+    constexpr int N = P3<K>::v;
+#pragma unroll
+    for (int f = K; f >= 1; f--) {
+#pragma unroll
+        for (int idx = 0; idx < N; idx++) {
+            if (fixed_digits(idx, K) == f) {
+                uint32_t kill = 0;
+#pragma unroll
+                for (int i = 0; i < K; i++) {
+                    const int s = pow3i(i);
+                    const int d = (idx / s) % 3;
+                    if (d != 2) kill |= v[idx + (2 - d) * s];
+                }
+                v[idx] &= ~kill;
+            }
+        }
+    }
+}
+
 // ternary index of the binary pattern b (bit k of b -> digit k)
 __host__ __device__ constexpr int bin_to_tern(int b) {
     int r = 0, p = 1;
