@@ -192,19 +192,20 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     constexpr int kMaxIter = 12;  // ceil(max warp range / 32): 3^7 blocks over 7 warps = 313 blocks
     __shared__ int64_t s_warp_off[kTileThreads / 32];
     __shared__ int64_t s_tile_off;
+    __shared__ uint8_t s_cnt[kTileThreads / 32][kMaxIter][32];  // block popcounts (<= 243)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
     const int nj = (b1 - b0 + 31) >> 5;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
 
-    // (1) lane = block: in-block axes (if any left for this pass) + popcount
-    int cj[kMaxIter];
+    // (1) lane = block: in-block axes (if any left for this pass), kills, popcount
+    //     (loops kept rolled: the kernel must stay inside the instruction cache)
     int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < kMaxIter; j++) {
-        cj[j] = 0;
-        if (j < nj) {
+#pragma unroll 1
+    for (int j = 0; j < nj; j++) {
+        int cj = 0;
+        {
             const int b = b0 + 32 * j + lane;
             if (b < b1) {
                 uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
@@ -231,11 +232,12 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                     q[0] = x0;
                     q[1] = x1;
                 }
-                cj[j] = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
-                        __popc(x1.z) + __popc(x1.w);
-                cnt += cj[j];
+                cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
+                     __popc(x1.z) + __popc(x1.w);
+                cnt += cj;
             }
         }
+        s_cnt[warp][j][lane] = (uint8_t)cj;
     }
     int wsum = cnt;
 #pragma unroll
@@ -266,10 +268,10 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     //     by shuffles) and that block's (q - excl)-th set bit, so every warp
     //     store writes 32 consecutive ranks.
     int64_t off = s_tile_off + s_warp_off[warp];
-#pragma unroll
-    for (int j = 0; j < kMaxIter; j++) {
-        if (j < nj) {
-            const int c = cj[j];
+#pragma unroll 1
+    for (int j = 0; j < nj; j++) {
+        {
+            const int c = s_cnt[warp][j][lane];
             if (__ballot_sync(0xffffffffu, c != 0) != 0u) {
                 int incl = c;
 #pragma unroll
