@@ -22,8 +22,10 @@
  *       expose the final bitmap in DenseState.words layout (h = 5,
  *       dense.py:127-170) for bitmap-level parity and k-GPU checks.
  *
- * Plain pointers and sizes only; no torch or CUDA types in signatures
- * (streams are passed as void*; NULL = the library's own stream).
+ * Plain pointers and sizes only; no torch or CUDA types in signatures.
+ * Device-buffer entry points take a cudaStream_t as void* and use it as
+ * given (0 = the legacy default stream, the CUDA convention; torch's default
+ * stream is that handle). Host-buffer entry points run on a private stream.
  * All host-buffer entry points are synchronous: results are complete on
  * return, as the reference's Python call is (SURVEY.md §8(b) "Threading").
  */

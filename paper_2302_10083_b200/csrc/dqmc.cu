@@ -1640,7 +1640,7 @@ int dqmc_primes_device(const void *input_dev, int in_kind, int n, int64_t *ranks
     if ((rc = ensure_attrs())) return rc;
     const Plan p = make_plan(n);
     if ((rc = check_cap(n, 0, 0, engine_device_bytes(p, flags & DQMC_FLAG_KEEP_BITMAP)))) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     if (!ranks_dev) flags |= DQMC_FLAG_COUNT_ONLY;
     return primes_device_impl(input_dev, in_kind, n, ranks_dev, ranks_cap, count_out, flags, s);
 }
@@ -1683,7 +1683,7 @@ int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, doubl
     if (!values_dev || x0 < 0 || count < 0) return set_err(DQMC_ERR_INVALID, "bad generator range");
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     // int(p * 2^53) as Python computes it (float64 product, truncation)
     const uint64_t t_on = (uint64_t)(p_on * 9007199254740992.0);
     const uint64_t t_any = (uint64_t)((p_on + p_dc) * 9007199254740992.0);
@@ -1708,7 +1708,7 @@ int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     const Plan p = make_plan(n);
     const uint32_t *tt32 = nullptr;
     if ((rc = input_words(input_dev, in_kind, n, &tt32, s))) return rc;
@@ -1727,7 +1727,7 @@ int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     const Plan p = make_plan(n);
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0 || ranks_dev == nullptr;
     Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
@@ -1746,7 +1746,7 @@ int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint6
         return set_err(DQMC_ERR_INVALID, "bitop: null pointer, size not a multiple of 16, or bad op");
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : g_eng.stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     const int64_t n16 = (int64_t)(nbytes / 16);
     const int grid = (int)std::min<int64_t>((n16 + 255) / 256, 148ll * 16);
     if (n16) k_bitop<<<grid, 256, 0, s>>>((uint4 *)dst, (const uint4 *)a, (const uint4 *)b, n16, op);

@@ -145,7 +145,18 @@ def test_gpu_emulated_shards_bit_exact(n, k, pkg, gen_mod):
     vd = device.gen3_device(n, 0.75, 0.05, 3)
     got = S.gpu_sharded_prime_ranks_emulated(vd, n, k)
     want = pkg.prime_ranks_from_values(vd.cpu().numpy())
-    assert np.array_equal(got, want)
+    assert np.array_equal(got, want), _block_diff(got, want, n, k)
+
+
+def _block_diff(got, want, n, k):
+    nl = n - k
+    out = [f"total got {len(got)} want {len(want)}"]
+    for t in S.all_blocks(k):
+        lo, hi = S.rho(t) * 3**nl, (S.rho(t) + 1) * 3**nl
+        g, w = got[(got >= lo) & (got < hi)], want[(want >= lo) & (want < hi)]
+        if not np.array_equal(g, w):
+            out.append(f"block {t}: got {len(g)} want {len(w)} missing {len(np.setdiff1d(w, g))} extra {len(np.setdiff1d(g, w))}")
+    return "; ".join(out)
 
 
 @pytest.mark.gpu
@@ -159,5 +170,7 @@ def test_gpu_emulated_config4_k3(pkg, golden):
     g = golden["configs"]["4"]
     vd = device.gen3_device(24, 0.75, 0.05, 3)
     got = S.gpu_sharded_prime_ranks_emulated(vd, 24, 3)
-    assert len(got) == g["primes"]
+    if len(got) != g["primes"]:
+        want = pkg.prime_ranks_from_values(vd.cpu().numpy())
+        raise AssertionError(_block_diff(got, want, 24, 3))
     assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()[:16] == g["ranks_sha256_prefix"]
