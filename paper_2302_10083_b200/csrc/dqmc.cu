@@ -17,6 +17,7 @@
 //                          warp-aggregated popcount, decoupled look-back scan
 //                          and ordered compaction to int64 ranks.
 // Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
+#include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -338,6 +339,12 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__
         run += cnt[i];
     }
     if (t == blockDim.x - 1) *total = s_part[t];
+}
+
+// total = pos[n-1] + cnt[n-1] after the exclusive scan
+__global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos, int64_t n,
+                             int64_t *total) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *total = n ? pos[n - 1] + cnt[n - 1] : 0;
 }
 
 // Copy every tile's ranks from its scratch range to its rank-order position
@@ -965,6 +972,8 @@ struct Engine {
     size_t scratch_cap = 0, scratch_want = 0;  // entries
     unsigned long long *alloc = nullptr;
     int64_t *total = nullptr;
+    void *cub_tmp = nullptr;
+    size_t cub_tmp_cap = 0;
     uint32_t *tt_tmp = nullptr;
     size_t tt_tmp_cap = 0;  // bytes
     void *in_tmp = nullptr;
@@ -1292,8 +1301,20 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
         if ((rc = launch_c0_final(p.g, ntiles, state, fa, s))) return rc;
         tm.mark("k_c0_final", S + (kill ? S : 0) + (bitmap_out ? S : 0));
     }
-    k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
-    CK(cudaGetLastError());
+    if (ntiles <= 4096) {
+        k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
+        CK(cudaGetLastError());
+    } else {
+        // device-wide exclusive scan (CUB) of the int32 counts into int64 positions
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int)ntiles, s));
+        if ((rc = grow(g_eng.cub_tmp, g_eng.cub_tmp_cap, tmp, 1))) return rc;
+        CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int)ntiles, s));
+        k_scan_total<<<1, 32, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
+        CK(cudaGetLastError());
+    }
     tm.mark("k_scan_tiles", (uint64_t)ntiles * 12);
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
@@ -1784,6 +1805,7 @@ void dqmc_release(void) {
     cudaFree(g_eng.tile_cnt);
     cudaFree(g_eng.scratch);
     cudaFree(g_eng.alloc);
+    cudaFree(g_eng.cub_tmp);
     cudaFree(g_eng.total);
     cudaFree(g_eng.tt_tmp);
     cudaFree(g_eng.in_tmp);
