@@ -1301,7 +1301,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
         if ((rc = launch_c0_final(p.g, ntiles, state, fa, s))) return rc;
         tm.mark("k_c0_final", S + (kill ? S : 0) + (bitmap_out ? S : 0));
     }
-    if (ntiles <= 4096) {
+    if (ntiles <= 4096 || getenv("DQMC_NO_CUB")) {
         k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
         CK(cudaGetLastError());
     } else {
