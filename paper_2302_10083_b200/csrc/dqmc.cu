@@ -180,6 +180,7 @@ struct FinalArgs {
     unsigned long long *alloc;  // running scratch allocation counter
     int64_t *tile_base;         // per tile: offset of its ranks in out
     int32_t *tile_cnt;          // per tile: prime count
+    int64_t tile0;              // first tile of this launch (chunked final stage)
 };
 
 
@@ -341,6 +342,12 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__
     if (t == blockDim.x - 1) *total = s_part[t];
 }
 
+// chunk pipeline: next = cur + pos[last] + cnt[last] (device-side running base)
+__global__ void k_chunk_advance(const int32_t *__restrict__ cnt_last, const int64_t *__restrict__ pos_last,
+                                int64_t *base) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) base[1] = base[0] + *pos_last + *cnt_last;
+}
+
 // total = pos[n-1] + cnt[n-1] after the exclusive scan
 __global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos, int64_t n,
                              int64_t *total) {
@@ -352,13 +359,14 @@ __global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__r
 __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
                                                  const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
                                                  int64_t *__restrict__ out, int64_t cap, int64_t ntiles,
-                                                 int64_t scap) {
+                                                 int64_t scap, const int64_t *__restrict__ dbase = nullptr) {
     const int lane = threadIdx.x & 31;
+    const int64_t add = dbase ? *dbase : 0;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
     for (int64_t t = w; t < ntiles; t += nw) {
         const int c = cnt[t];
-        const int64_t src = base[t], dst = pos[t];
+        const int64_t src = base[t], dst = pos[t] + add;
         // a tile whose range overflowed the scratch is skipped: the host sees
         // total > scratch capacity, grows the scratch and reruns the final stage
         if (c < 0 || src < 0 || src + c > scap) continue;
@@ -498,7 +506,7 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__res
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     constexpr int NB = pow3i(G);
-    const int64_t tile = blockIdx.x;
+    const int64_t tile = blockIdx.x + fa.tile0;
     const int64_t blk0 = tile * NB;
     if (threadIdx.x == 0) {
         mbar_init(&mbar, 1);
@@ -956,8 +964,8 @@ int set_err(int code, const std::string &msg) {
     } while (0)
 
 struct PinnedBuf {
-    int64_t *ptr = nullptr;
-    size_t cap = 0;  // entries
+    int64_t *ptr = nullptr;  // mapped pinned host memory (UVA: also the device address)
+    size_t cap = 0;          // entries
 };
 
 struct Engine {
@@ -974,6 +982,11 @@ struct Engine {
     int64_t *total = nullptr;
     void *cub_tmp = nullptr;
     size_t cub_tmp_cap = 0;
+    cudaStream_t stream2 = nullptr;   // copy-out stream of the pipelined host API
+    cudaEvent_t chunk_ev[16] = {};
+    int64_t *chunk_base = nullptr;    // device running bases of the chunked final stage
+    int hint_n = -1;
+    int64_t hint_count = 0;           // prime count of the last host call (sizes the pinned output)
     uint32_t *tt_tmp = nullptr;
     size_t tt_tmp_cap = 0;  // bytes
     void *in_tmp = nullptr;
@@ -1005,6 +1018,9 @@ int ensure_device() {
     g_eng.device = dev;
     CK(cudaStreamCreateWithFlags(&g_eng.stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&g_eng.alloc, 256));
+    CK(cudaStreamCreateWithFlags(&g_eng.stream2, cudaStreamNonBlocking));
+    for (int i = 0; i < 16; i++) CK(cudaEventCreateWithFlags(&g_eng.chunk_ev[i], cudaEventDisableTiming));
+    CK(cudaMalloc(&g_eng.chunk_base, 17 * sizeof(int64_t)));
     CK(cudaMalloc(&g_eng.total, 256));
     return DQMC_OK;
 }
@@ -1292,6 +1308,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
     fa.alloc = g_eng.alloc;
     fa.tile_base = g_eng.tile_base;
     fa.tile_cnt = g_eng.tile_cnt;
+    fa.tile0 = 0;
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
     if (tt32) {
         k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
@@ -1527,7 +1544,7 @@ int alloc_pinned(size_t entries, PinnedBuf &out) {
     }
     size_t want = std::max<size_t>(entries, 1024);
     int64_t *p = nullptr;
-    cudaError_t e = cudaHostAlloc((void **)&p, want * 8, cudaHostAllocDefault);
+    cudaError_t e = cudaHostAlloc((void **)&p, want * 8, cudaHostAllocMapped);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         char buf[160];
@@ -1536,6 +1553,67 @@ int alloc_pinned(size_t entries, PinnedBuf &out) {
     }
     out.ptr = p;
     out.cap = want;
+    return DQMC_OK;
+}
+
+// Host-API final stage, pipelined: the tiles are finished in K chunks on the
+// compute stream; as soon as a chunk's ranks have positions, a copy-out
+// kernel on stream2 scatters them into mapped pinned host memory over PCIe
+// while the next chunk computes. Returns the total count; *host_ok is false if
+// the host buffer (sized from the previous call) was too small.
+int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int64_t host_cap, int64_t *count,
+                        bool *host_ok, cudaStream_t s) {
+    const int64_t ntiles = pow3l(p.T);
+    const int K = (int)std::min<int64_t>(8, ntiles);
+    int rc;
+    if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+        FinalArgs fa;
+        fa.out = g_eng.scratch;
+        fa.cap = (int64_t)g_eng.scratch_cap;
+        fa.rank_add = -p.rank_sub;
+        fa.kill = nullptr;
+        fa.ib_mask = p.ib_E;
+        fa.bitmap_out = nullptr;
+        fa.alloc = g_eng.alloc;
+        fa.tile_base = g_eng.tile_base;
+        fa.tile_cnt = g_eng.tile_cnt;
+        CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
+        CK(cudaMemsetAsync(g_eng.chunk_base, 0, 8, s));
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int)((ntiles + K - 1) / K + 1), s));
+        if ((rc = grow(g_eng.cub_tmp, g_eng.cub_tmp_cap, tmp, 1))) return rc;
+        for (int c = 0; c < K; c++) {
+            const int64_t t0 = ntiles * c / K, t1 = ntiles * (c + 1) / K;
+            fa.tile0 = t0;
+            if ((rc = launch_c0_final(p.g, t1 - t0, state, fa, s))) return rc;
+            CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt + t0, g_eng.tile_pos + t0, cub::Sum(),
+                                              (int64_t)0, (int)(t1 - t0), s));
+            k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(g_eng.chunk_ev[c], s));
+            CK(cudaStreamWaitEvent(g_eng.stream2, g_eng.chunk_ev[c], 0));
+            const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 2);
+            k_reorder<<<grid, 256, 0, g_eng.stream2>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
+                                                       g_eng.tile_pos + t0, host, host_cap, t1 - t0,
+                                                       (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
+            CK(cudaGetLastError());
+        }
+        int64_t vals[2] = {0, 0};
+        CK(cudaMemcpyAsync(&vals[0], g_eng.chunk_base + K, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&vals[1], g_eng.alloc, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(g_eng.stream2));
+        *count = vals[0];
+        if ((size_t)vals[1] <= g_eng.scratch_cap) break;
+        g_eng.scratch_want = (size_t)((double)vals[1] * 1.05) + 1024;  // scratch overflow: once more
+    }
+    *host_ok = *count <= host_cap;
     return DQMC_OK;
 }
 
@@ -1559,6 +1637,36 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
     if ((rc = grow(g_eng.in_tmp, g_eng.in_tmp_cap, std::max<size_t>(in_bytes, 8), 1))) return rc;
     CK(cudaMemcpyAsync(g_eng.in_tmp, host_in, in_bytes, cudaMemcpyHostToDevice, s));
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0;
+    const bool pipelined = !count_only && !(flags & (DQMC_FLAG_KEEP_BITMAP | DQMC_FLAG_TIMING)) && p.T > 0 &&
+                           g_eng.hint_n == n && g_eng.hint_count > 0 && !getenv("DQMC_NO_PIPELINE");
+    if (pipelined) {
+        // merge/reduce passes, then the chunked final stage straight into pinned host memory
+        const uint32_t *tt32 = nullptr;
+        if ((rc = input_words(g_eng.in_tmp, kind, n, &tt32, s))) return rc;
+        if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.nblocks * 32, 1))) return rc;
+        Timer tm{false, s};
+        if ((rc = run_merge(p, tt32, g_eng.state, false, tm, s))) return rc;
+        if ((rc = run_reduce(p, g_eng.state, true, tm, s))) return rc;
+        PinnedBuf pb;
+        if ((rc = alloc_pinned((size_t)((double)g_eng.hint_count * 1.02) + 4096, pb))) return rc;
+        int64_t count = 0;
+        bool ok = true;
+        if ((rc = run_final_pipelined(p, g_eng.state, pb.ptr, (int64_t)pb.cap, &count, &ok, s))) return rc;
+        if (!ok) {  // the output outgrew the hinted buffer: rerun the stage into a larger one
+            g_eng.free_pinned.push_back(pb);
+            if ((rc = alloc_pinned((size_t)count, pb))) return rc;
+            if ((rc = run_final_pipelined(p, g_eng.state, pb.ptr, (int64_t)pb.cap, &count, &ok, s))) return rc;
+        }
+        g_eng.hint_count = count;
+        out->count = count;
+        if (count > 0) {
+            out->ranks = pb.ptr;
+            out->_owner = new PinnedBuf(pb);
+        } else {
+            g_eng.free_pinned.push_back(pb);
+        }
+        return DQMC_OK;
+    }
     if (!count_only && g_eng.ranks_cap == 0) {
         if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)1 << 20, 8))) return rc;
     }
@@ -1573,6 +1681,10 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
             return rc;
     }
     out->count = count;
+    if (!count_only) {
+        g_eng.hint_n = n;
+        g_eng.hint_count = count;
+    }
     if (!count_only && count > 0) {
         PinnedBuf pb;
         if ((rc = alloc_pinned((size_t)count, pb))) return rc;
@@ -1812,6 +1924,10 @@ void dqmc_release(void) {
     cudaFree(g_eng.ranks);
     for (auto &b : g_eng.free_pinned) cudaFreeHost(b.ptr);
     if (g_eng.stream) cudaStreamDestroy(g_eng.stream);
+    if (g_eng.stream2) cudaStreamDestroy(g_eng.stream2);
+    for (int i = 0; i < 16; i++)
+        if (g_eng.chunk_ev[i]) cudaEventDestroy(g_eng.chunk_ev[i]);
+    cudaFree(g_eng.chunk_base);
     g_eng = Engine();
 }
 

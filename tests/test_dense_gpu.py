@@ -128,6 +128,25 @@ class TestContract:
         assert np.array_equal(outs[0], again) and len(small) > 0
 
 
+class TestPipelinedHostPath:
+    @pytest.mark.parametrize("n", [13, 17, 20])
+    def test_pipelined_equals_plain(self, pkg, oracle_mod, gen_mod, n, monkeypatch):
+        """The host API pipelines the final stage (chunked, copied out over
+        PCIe while the next chunk computes) once it has a size hint."""
+        v = gen_mod.gen3(n, 0.8, 0.05, 11)
+        want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
+        first = pkg.prime_ranks_from_values(v)  # sets the hint
+        second = pkg.prime_ranks_from_values(v)  # pipelined
+        monkeypatch.setenv("DQMC_NO_PIPELINE", "1")
+        plain = pkg.prime_ranks_from_values(v)
+        assert np.array_equal(first, want) and np.array_equal(second, want) and np.array_equal(plain, want)
+        # a larger output than the hint (grow path): denser table, same n
+        monkeypatch.delenv("DQMC_NO_PIPELINE")
+        v2 = gen_mod.gen3(n, 0.95, 0.0, 12)
+        got = pkg.prime_ranks_from_values(v2)
+        assert np.array_equal(got, oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v2), n))
+
+
 class TestDevice:
     def test_gen3_device_matches_oracle(self, pkg, gen_mod):
         from paper_2302_10083_b200 import device
