@@ -344,8 +344,13 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__
 
 // chunk pipeline: next = cur + pos[last] + cnt[last] (device-side running base)
 __global__ void k_chunk_advance(const int32_t *__restrict__ cnt_last, const int64_t *__restrict__ pos_last,
-                                int64_t *base) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) base[1] = base[0] + *pos_last + *cnt_last;
+                                int64_t *base, volatile int64_t *host_mirror) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const int64_t b0 = base[0], b1 = b0 + *pos_last + *cnt_last;
+        base[1] = b1;
+        host_mirror[0] = b0;  // mapped pinned memory: the host reads it after the chunk event
+        host_mirror[1] = b1;
+    }
 }
 
 // total = pos[n-1] + cnt[n-1] after the exclusive scan
@@ -983,8 +988,9 @@ struct Engine {
     void *cub_tmp = nullptr;
     size_t cub_tmp_cap = 0;
     cudaStream_t stream2 = nullptr;   // copy-out stream of the pipelined host API
-    cudaEvent_t chunk_ev[16] = {};
+    cudaEvent_t chunk_ev[17] = {};
     int64_t *chunk_base = nullptr;    // device running bases of the chunked final stage
+    int64_t *hbase = nullptr;         // mapped pinned host mirror of chunk_base
     int hint_n = -1;
     int64_t hint_count = 0;           // prime count of the last host call (sizes the pinned output)
     uint32_t *tt_tmp = nullptr;
@@ -1021,6 +1027,7 @@ int ensure_device() {
     CK(cudaStreamCreateWithFlags(&g_eng.stream2, cudaStreamNonBlocking));
     for (int i = 0; i < 16; i++) CK(cudaEventCreateWithFlags(&g_eng.chunk_ev[i], cudaEventDisableTiming));
     CK(cudaMalloc(&g_eng.chunk_base, 17 * sizeof(int64_t)));
+    CK(cudaHostAlloc((void **)&g_eng.hbase, 17 * sizeof(int64_t), cudaHostAllocMapped));
     CK(cudaMalloc(&g_eng.total, 256));
     return DQMC_OK;
 }
@@ -1544,7 +1551,7 @@ int alloc_pinned(size_t entries, PinnedBuf &out) {
     }
     size_t want = std::max<size_t>(entries, 1024);
     int64_t *p = nullptr;
-    cudaError_t e = cudaHostAlloc((void **)&p, want * 8, cudaHostAllocMapped);
+    cudaError_t e = cudaHostAlloc((void **)&p, want * 8, cudaHostAllocDefault);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         char buf[160];
@@ -1557,18 +1564,21 @@ int alloc_pinned(size_t entries, PinnedBuf &out) {
 }
 
 // Host-API final stage, pipelined: the tiles are finished in K chunks on the
-// compute stream; as soon as a chunk's ranks have positions, a copy-out
-// kernel on stream2 scatters them into mapped pinned host memory over PCIe
-// while the next chunk computes. Returns the total count; *host_ok is false if
-// the host buffer (sized from the previous call) was too small.
+// compute stream (E, scan, running base, reorder into the device rank
+// buffer); as soon as chunk c's event fires the host queues its D2H copy on
+// the copy stream, so the copy engine moves chunk c while the SMs finish
+// chunk c+1. Returns the total; *host_ok is false if the host buffer (sized
+// from the previous call) was too small.
 int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int64_t host_cap, int64_t *count,
                         bool *host_ok, cudaStream_t s) {
     const int64_t ntiles = pow3l(p.T);
-    const int K = (int)std::min<int64_t>(8, ntiles);
+    const int K = (int)std::min<int64_t>(16, ntiles);
     int rc;
     if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)host_cap, 8))) return rc;
+    int64_t *hbase = g_eng.hbase;  // mapped pinned mirror of the chunk bases
     for (int attempt = 0; attempt < 2; attempt++) {
         const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
         if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
@@ -1594,26 +1604,35 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
             if ((rc = launch_c0_final(p.g, t1 - t0, state, fa, s))) return rc;
             CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt + t0, g_eng.tile_pos + t0, cub::Sum(),
                                               (int64_t)0, (int)(t1 - t0), s));
-            k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c);
+            k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c,
+                                             hbase + c);
+            CK(cudaGetLastError());
+            const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 8);
+            k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
+                                           g_eng.tile_pos + t0, g_eng.ranks, host_cap, t1 - t0,
+                                           (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
             CK(cudaGetLastError());
             CK(cudaEventRecord(g_eng.chunk_ev[c], s));
-            CK(cudaStreamWaitEvent(g_eng.stream2, g_eng.chunk_ev[c], 0));
-            const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 2);
-            k_reorder<<<grid, 256, 0, g_eng.stream2>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
-                                                       g_eng.tile_pos + t0, host, host_cap, t1 - t0,
-                                                       (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
-            CK(cudaGetLastError());
         }
-        int64_t vals[2] = {0, 0};
-        CK(cudaMemcpyAsync(&vals[0], g_eng.chunk_base + K, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(&vals[1], g_eng.alloc, 8, cudaMemcpyDeviceToHost, s));
+        // copy-out as chunks complete (copy engine, overlapped with later chunks)
+        bool fits = true;
+        for (int c = 0; c < K; c++) {
+            CK(cudaEventSynchronize(g_eng.chunk_ev[c]));
+            const int64_t lo = hbase[c], hi = hbase[c + 1];
+            if (hi > host_cap) fits = false;
+            if (fits && hi > lo)
+                CK(cudaMemcpyAsync(host + lo, g_eng.ranks + lo, (size_t)(hi - lo) * 8, cudaMemcpyDeviceToHost,
+                                   g_eng.stream2));
+        }
+        int64_t used = 0;
+        CK(cudaMemcpyAsync(&used, g_eng.alloc, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         CK(cudaStreamSynchronize(g_eng.stream2));
-        *count = vals[0];
-        if ((size_t)vals[1] <= g_eng.scratch_cap) break;
-        g_eng.scratch_want = (size_t)((double)vals[1] * 1.05) + 1024;  // scratch overflow: once more
+        *count = hbase[K];
+        *host_ok = fits && *count <= host_cap;
+        if ((size_t)used <= g_eng.scratch_cap) break;
+        g_eng.scratch_want = (size_t)((double)used * 1.05) + 1024;  // scratch overflow: once more
     }
-    *host_ok = *count <= host_cap;
     return DQMC_OK;
 }
 
@@ -1928,6 +1947,7 @@ void dqmc_release(void) {
     for (int i = 0; i < 16; i++)
         if (g_eng.chunk_ev[i]) cudaEventDestroy(g_eng.chunk_ev[i]);
     cudaFree(g_eng.chunk_base);
+    if (g_eng.hbase) cudaFreeHost(g_eng.hbase);
     g_eng = Engine();
 }
 
