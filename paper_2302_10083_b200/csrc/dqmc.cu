@@ -901,6 +901,134 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     }
 }
 
+// MERGE_REDUCE pass with decoupled resources: the 2^R binary-row gathers land
+// in two small stage buffers (load warp), the finished 3^R-row tiles leave
+// from two tile buffers (store warp). A gather never waits for a tile store,
+// so the compute warps always find the next item's rows ready.
+template <int R1, int R2>
+__global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
+    k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
+                        int64_t ncol, int64_t nitems, uint32_t ib_mask) {
+    using SM = PipeSmem<R1, R2>;
+    constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
+    constexpr int NR = SM::NR;
+    constexpr int CW = SM::CW;
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ __align__(8) uint64_t stage_full[2], stage_free[2], tile_done[2], tile_free[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&stage_full[b], 1);
+            mbar_init(&stage_free[b], CW);
+            mbar_init(&tile_done[b], CW);
+            mbar_init(&tile_free[b], 1);
+        }
+    }
+    __syncthreads();
+
+    if (warp == CW) {  // ---------------------------------- load warp
+        if (lane == 0) {
+            for (int64_t i = 0; i < L; i++) {
+                const int b = (int)(i & 1);
+                if (i >= 2) mbar_wait(&stage_free[b], (unsigned)(((i - 2) >> 1) & 1));
+                const int64_t it = blockIdx.x + i * gridDim.x;
+                const int c0 = (int)((it % ncol) * 32);
+                uint32_t *st = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
+                mbar_expect_tx(&stage_full[b], SM::STAGE_WORDS * 4);
+#pragma unroll
+                for (int b2 = 0; b2 < B2; b2++)
+                    tma_load_5d(st + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &stage_full[b]);
+            }
+        }
+        return;
+    }
+    if (warp == CW + 1) {  // ------------------------------ store warp
+        if (lane == 0) {
+            for (int64_t i = 0; i < L; i++) {
+                const int b = (int)(i & 1);
+                const int64_t it = blockIdx.x + i * gridDim.x;
+                mbar_wait(&tile_done[b], (unsigned)((i >> 1) & 1));
+                const uint32_t *tile = smem + b * SM::TILE_WORDS;
+                const int c0 = (int)((it % ncol) * 32);
+#pragma unroll
+                for (int x = 0; x < SM::NBOX; x++) tma_store_3d(&tmap, c0, x * SM::BOXR, 0, tile + x * SM::BOXR * 32);
+                bulk_commit();
+                bulk_wait_read0();
+                mbar_arrive(&tile_free[b]);
+            }
+            bulk_wait0();
+        }
+        return;
+    }
+
+    // ---------------------------------------------- compute warps
+    constexpr int NCT = CW * 32;
+    for (int64_t i = 0; i < L; i++) {
+        const int b = (int)(i & 1);
+        const int tb = b * SM::TILE_WORDS;
+        const int sb = 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
+        mbar_wait(&stage_full[b], (unsigned)((i >> 1) & 1));
+        if (i >= 2) mbar_wait(&tile_free[b], (unsigned)(((i - 2) >> 1) & 1));
+        // round 1: merge the R1 axes for each binary rho2 (stage -> tile)
+        for (int t2 = warp; t2 < B2; t2 += CW) {
+            const int r2 = bin_to_tern(t2);
+            uint32_t v[N1];
+#pragma unroll
+            for (int x = 0; x < N1; x++) v[x] = 0;
+#pragma unroll
+            for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * 32 + lane];
+            cube_merge<R1>(v);
+            if (R2 == 0) cube_reduce_par<R1>(v);
+#pragma unroll
+            for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * 32 + lane] = v[x];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stage_free[b]);
+        if (R2 > 0) {
+            bar_compute(NCT);
+            for (int t1 = warp; t1 < N1; t1 += CW) {
+                uint32_t v[N2];
+#pragma unroll
+                for (int x = 0; x < N2; x++) v[x] = 0;
+#pragma unroll
+                for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * 32 + lane];
+                cube_merge<R2>(v);
+                cube_reduce_par<R2>(v);
+#pragma unroll
+                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
+            }
+            bar_compute(NCT);
+            for (int t2 = warp; t2 < N2; t2 += CW) {
+                uint32_t v[N1];
+#pragma unroll
+                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
+                cube_reduce_par<R1>(v);
+#pragma unroll
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
+            }
+        }
+        if (ib_mask) {
+            bar_compute(NCT);
+            const int h = (lane >> 2) & 1;
+            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, ib_mask);
+                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
+                p[h] = h ? z1 : z0;
+                p[h ^ 1] = h ? z0 : z1;
+            }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_done[b]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -1067,6 +1195,13 @@ int set_pipe_attr() {
     return DQMC_OK;
 }
 
+template <int R1, int R2>
+int set_mr_attr() {
+    using SM = PipeSmem<R1, R2>;
+    CK(cudaFuncSetAttribute(k_merge_reduce_pipe<R1, R2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::SMEM));
+    return DQMC_OK;
+}
+
 template <int MODE>
 int set_pipe_attrs() {
     int rc;
@@ -1103,6 +1238,9 @@ int ensure_attrs() {
     if ((rc = set_mode_attrs<REDUCE_ONLY>())) return rc;
     if ((rc = set_pipe_attrs<MERGE_REDUCE>())) return rc;
     if ((rc = set_pipe_attrs<REDUCE_ONLY>())) return rc;
+    if ((rc = set_mr_attr<1, 0>()) || (rc = set_mr_attr<2, 0>()) || (rc = set_mr_attr<3, 0>()) ||
+        (rc = set_mr_attr<2, 2>()) || (rc = set_mr_attr<3, 2>()) || (rc = set_mr_attr<3, 3>()))
+        return rc;
     CK(cudaDeviceGetAttribute(&g_eng.num_sms, cudaDevAttrMultiProcessorCount, g_eng.device));
     g_eng.attrs_set = true;
     return DQMC_OK;
@@ -1225,7 +1363,10 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     }
     const int64_t nitems = ncol * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
-    k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
+    if (MODE == MERGE_REDUCE)
+        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
+    else
+        k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
     CK(cudaGetLastError());
     return DQMC_OK;
 }
