@@ -218,28 +218,32 @@ def run_engine_bench(args):
         device.dense_prime_ranks_device(values, n, out=out)
     torch.cuda.synchronize()
 
-    # ---- value: device-resident, CUDA events on the launching stream
+    # ---- value: device-resident, CUDA events on the launching stream (no per-pass timing)
     stream = torch.cuda.current_stream(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    pass_times: dict[str, list[float]] = {}
-    pass_bytes: dict[str, int] = {}
-    launches = 0
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            _, c = device.dense_prime_ranks_device(values, n, out=out, timing=True)
-            assert c == cnt
-            tl = _lib.timings()
-            launches += len(tl) + 1  # + the uint8 -> bit packing kernel
-            for name, ms, by in tl:
-                pass_times.setdefault(name, []).append(ms)
-                pass_bytes[name] = by
+            _, c = device.dense_prime_ranks_device(values, n, out=out)
         ev1.record(stream)
         torch.cuda.synchronize()
+    assert c == cnt
     t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
     value = 3**n / t_step
+
+    # ---- per-pass breakdown (CUDA events around every pass, separate loop)
+    pass_times: dict[str, list[float]] = {}
+    pass_bytes: dict[str, int] = {}
+    launches = 0
+    for _ in range(args.steps):
+        device.dense_prime_ranks_device(values, n, out=out, timing=True)
+        tl = _lib.timings()
+        launches += len(tl) + 1  # + the uint8 -> bit packing kernel
+        for name, ms, by in tl:
+            pass_times.setdefault(name, []).append(ms)
+            pass_bytes[name] = by
 
     # dominant kernel (largest share of the step)
     tot = {k: sum(v) for k, v in pass_times.items()}
