@@ -728,44 +728,6 @@ __device__ __forceinline__ void bar_compute(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-// In-block axes of a strided tile, sparse: all-zero blocks stay zero under
-// REDUCE, so each warp first compacts the indices of its nonzero blocks
-// (ballot + popc, 2 LDS.128 per block), then runs the shift/LOP3 kills only on
-// those, 32 per step with every lane busy. Cost follows the nonzero blocks.
-__device__ __forceinline__ void inblock_round_sparse(uint32_t *smem, int tb, int nblk, uint32_t ib_mask, int warp,
-                                                     int nwarps, uint16_t *list) {
-    const int lane = threadIdx.x & 31;
-    const int h = (lane >> 2) & 1;
-    const int b0 = nblk * warp / nwarps, b1 = nblk * (warp + 1) / nwarps;
-    int cnt = 0;
-    for (int base = b0; base < b1; base += 32) {
-        const int b = base + lane;
-        bool nz = false;
-        if (b < b1) {
-            const uint4 *p = reinterpret_cast<const uint4 *>(&smem[tb + b * 8]);
-            const uint4 ya = p[h], yb = p[h ^ 1];
-            nz = (ya.x | ya.y | ya.z | ya.w | yb.x | yb.y | yb.z | yb.w) != 0u;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, nz);
-        if (nz) list[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)b;
-        cnt += __popc(m);
-    }
-    __syncwarp();
-    for (int i = 0; i < cnt; i += 32) {
-        if (i + lane < cnt) {
-            const int b = list[i + lane];
-            uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + b * 8]);
-            const uint4 ya = p[h], yb = p[h ^ 1];
-            const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
-            uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            inblock_reduce(v, ib_mask);
-            const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
-            p[h] = h ? z1 : z0;
-            p[h ^ 1] = h ? z0 : z1;
-        }
-    }
-}
-
 template <int R1, int R2>
 struct PipeSmem {
     static constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v;
@@ -799,7 +761,6 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     constexpr int CW = SM::CW;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t full[2], computed[2];
-    __shared__ uint16_t s_list[CW][(NR * kRowBlocks + CW - 1) / CW + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
@@ -920,7 +881,19 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
         }
         if (ib_mask) {
             bar_compute(NCT);
-            inblock_round_sparse(smem, tb, NR * kRowBlocks, ib_mask, warp, CW, s_list[warp]);
+            // in-block axes, thread per block; halves swapped on lanes 4-7 of
+            // every 8 so each LDS.128/STS.128 quarter-warp hits 32 distinct banks
+            const int h = (lane >> 2) & 1;
+            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, ib_mask);
+                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
+                p[h] = h ? z1 : z0;
+                p[h ^ 1] = h ? z0 : z1;
+            }
         }
         fence_async_smem();
         __syncwarp();
@@ -942,7 +915,6 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     constexpr int CW = SM::CW;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t stage_full[2], stage_free[2], tile_done[2], tile_free[2];
-    __shared__ uint16_t s_list[CW][(NR * kRowBlocks + CW - 1) / CW + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
@@ -1039,7 +1011,17 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
         }
         if (ib_mask) {
             bar_compute(NCT);
-            inblock_round_sparse(smem, tb, NR * kRowBlocks, ib_mask, warp, CW, s_list[warp]);
+            const int h = (lane >> 2) & 1;
+            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                inblock_reduce(v, ib_mask);
+                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
+                p[h] = h ? z1 : z0;
+                p[h ^ 1] = h ? z0 : z1;
+            }
         }
         fence_async_smem();
         __syncwarp();
