@@ -883,16 +883,16 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             bar_compute(NCT);
             // in-block axes, thread per block; halves swapped on lanes 4-7 of
             // every 8 so each LDS.128/STS.128 quarter-warp hits 32 distinct banks
-            const int h = (lane >> 2) & 1;
+            // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
+            // MIO wavefronts, which have slack here; a lane half-swap would cost
+            // 16 ALU selects per block on the saturated ALU pipe)
             for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
                 uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
-                const uint4 ya = p[h], yb = p[h ^ 1];
-                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                const uint4 x0 = p[0], x1 = p[1];
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
                 inblock_reduce(v, ib_mask);
-                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
-                p[h] = h ? z1 : z0;
-                p[h ^ 1] = h ? z0 : z1;
+                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
             }
         }
         fence_async_smem();
@@ -1011,16 +1011,16 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
         }
         if (ib_mask) {
             bar_compute(NCT);
-            const int h = (lane >> 2) & 1;
+            // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
+            // MIO wavefronts, which have slack here; a lane half-swap would cost
+            // 16 ALU selects per block on the saturated ALU pipe)
             for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
                 uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
-                const uint4 ya = p[h], yb = p[h ^ 1];
-                const uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                const uint4 x0 = p[0], x1 = p[1];
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
                 inblock_reduce(v, ib_mask);
-                const uint4 z0 = make_uint4(v[0], v[1], v[2], v[3]), z1 = make_uint4(v[4], v[5], v[6], v[7]);
-                p[h] = h ? z1 : z0;
-                p[h ^ 1] = h ? z0 : z1;
+                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
             }
         }
         fence_async_smem();
