@@ -34,6 +34,8 @@ def short(name: str) -> str:
         return name
     base = m.group(1)
     tmpl = m.group(2) or ""
+    if base == "k_merge_reduce_pipe":
+        return "k_strided<MERGE_REDUCE>"
     if base == "k_strided_pipe":
         mode = tmpl.strip("<>").split(",")[-1].strip()
         return {"1": "k_strided<MERGE_REDUCE>", "2": "k_strided<REDUCE>"}.get(mode, base + tmpl)
