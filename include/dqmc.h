@@ -18,9 +18,13 @@
  *       errors.py:23-24).
  *   DQMC_ERR_INVALID
  *       replaces ValueError for a bad split h (dense.py:356-357) or n.
- *   dqmc_state_device / dqmc_state_download
+ *   dqmc_bitmap_device / dqmc_bitmap_download
  *       expose the final bitmap in DenseState.words layout (h = 5,
  *       dense.py:127-170) for bitmap-level parity and k-GPU checks.
+ *   dqmc_state_* (device-resident DenseState, any split h)
+ *       replace load / DenseState.run_pass / run_merge_reduce /
+ *       padding_bits_zero / equal_state / copy / extract_ranks,
+ *       dense.py:127-397.
  *
  * Plain pointers and sizes only; no torch or CUDA types in signatures.
  * Device-buffer entry points take a cudaStream_t as void* and use it as
@@ -101,10 +105,30 @@ int dqmc_last_pass_bytes(uint64_t *bytes, int max);
 
 /* Device pointer of the engine's state (reference layout, h = 5) after a
  * call with DQMC_FLAG_KEEP_BITMAP, and its size in bytes. */
-int dqmc_state_device(void **ptr, uint64_t *bytes);
+int dqmc_bitmap_device(void **ptr, uint64_t *bytes);
 
-/* Copy the device state to a host buffer of dqmc_state_bytes(n, 5) bytes. */
-int dqmc_state_download(void *host, uint64_t bytes);
+/* Copy that final bitmap to a host buffer of dqmc_state_bytes(n, 5) bytes. */
+int dqmc_bitmap_download(void *host, uint64_t bytes);
+
+/* Device-resident DenseState for any split h (dense.py:127-397), one
+ * streaming kernel per dimension exactly like the reference's layers
+ * (dqmc_state.cu). op: 0 = MERGE, 1 = REDUCE. dims are 1-based; counts get
+ * 3^(n-h-1) block-triples for top dims, -1 for in-block dims (run_pass's
+ * return value). dqmc_state_extract returns DQMC_ERR_INVALID if a padding bit
+ * is set (the reference's AssertionError); ranks_host may be NULL to count. */
+typedef struct dqmc_state dqmc_state_t;
+int dqmc_state_create(int n, int h, uint64_t mem_cap, dqmc_state_t **out);
+void dqmc_state_free(dqmc_state_t *st);
+int dqmc_state_info(const dqmc_state_t *st, int64_t *out5);  /* n, h, block_bits, blocks, words */
+int dqmc_state_load_tt(dqmc_state_t *st, const uint64_t *tt_words_host);
+int dqmc_state_set_words(dqmc_state_t *st, const uint64_t *words, uint64_t nwords);
+int dqmc_state_get_words(const dqmc_state_t *st, uint64_t *words, uint64_t nwords);
+int dqmc_state_run_pass(dqmc_state_t *st, int op, const int *dims, int ndims, int64_t *counts);
+int dqmc_state_run_merge_reduce(dqmc_state_t *st);
+int dqmc_state_padding_zero(const dqmc_state_t *st, int *ok);
+int dqmc_state_extract(const dqmc_state_t *st, int64_t *ranks_host, int64_t cap, int64_t *count);
+int dqmc_state_equal(const dqmc_state_t *a, const dqmc_state_t *b, int *eq);
+int dqmc_state_copy(const dqmc_state_t *src, dqmc_state_t **out);
 
 /* Device-side synthetic inputs (frozen generator of ttio.py:331-378 and the
  * survey's 3-way / S-box variants); writes 2^n uint8. */

@@ -46,8 +46,8 @@ EXPORTS = (
     "dqmc_primes_device",
     "dqmc_last_timings",
     "dqmc_last_pass_bytes",
-    "dqmc_state_device",
-    "dqmc_state_download",
+    "dqmc_bitmap_device",
+    "dqmc_bitmap_download",
     "dqmc_gen3_device",
     "dqmc_gen3_range_device",
     "dqmc_merge_device",
@@ -55,6 +55,18 @@ EXPORTS = (
     "dqmc_bitop_device",
     "dqmc_plan",
     "dqmc_release",
+    "dqmc_state_create",
+    "dqmc_state_free",
+    "dqmc_state_info",
+    "dqmc_state_load_tt",
+    "dqmc_state_set_words",
+    "dqmc_state_get_words",
+    "dqmc_state_run_pass",
+    "dqmc_state_run_merge_reduce",
+    "dqmc_state_padding_zero",
+    "dqmc_state_extract",
+    "dqmc_state_equal",
+    "dqmc_state_copy",
 )
 
 
@@ -106,8 +118,20 @@ def load() -> ctypes.CDLL:
             "dqmc_primes_device": (i32, [vp, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),
             "dqmc_last_timings": (i32, [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), i32]),
             "dqmc_last_pass_bytes": (i32, [ctypes.POINTER(ctypes.c_uint64), i32]),
-            "dqmc_state_device": (i32, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)]),
-            "dqmc_state_download": (i32, [vp, u64]),
+            "dqmc_bitmap_device": (i32, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)]),
+            "dqmc_bitmap_download": (i32, [vp, u64]),
+            "dqmc_state_create": (i32, [i32, i32, u64, ctypes.POINTER(ctypes.c_void_p)]),
+            "dqmc_state_free": (None, [vp]),
+            "dqmc_state_info": (i32, [vp, ctypes.POINTER(ctypes.c_int64)]),
+            "dqmc_state_load_tt": (i32, [vp, vp]),
+            "dqmc_state_set_words": (i32, [vp, vp, u64]),
+            "dqmc_state_get_words": (i32, [vp, vp, u64]),
+            "dqmc_state_run_pass": (i32, [vp, i32, vp, i32, vp]),
+            "dqmc_state_run_merge_reduce": (i32, [vp]),
+            "dqmc_state_padding_zero": (i32, [vp, ctypes.POINTER(ctypes.c_int)]),
+            "dqmc_state_extract": (i32, [vp, vp, i64, ctypes.POINTER(ctypes.c_int64)]),
+            "dqmc_state_equal": (i32, [vp, vp, ctypes.POINTER(ctypes.c_int)]),
+            "dqmc_state_copy": (i32, [vp, ctypes.POINTER(ctypes.c_void_p)]),
             "dqmc_gen3_device": (i32, [vp, i32, dbl, dbl, u64, vp]),
             "dqmc_gen3_range_device": (i32, [vp, i64, i64, dbl, dbl, u64, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),

@@ -1862,6 +1862,9 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
 // ---------------------------------------------------------------------------
 // C ABI
 
+// shared error channel of the state API (dqmc_state.cu); not part of the ABI
+extern "C" __attribute__((visibility("hidden"))) void dqmc_internal_set_error(const char *m) { g_err = m; }
+
 extern "C" {
 
 int dqmc_abi_version(void) { return DQMC_ABI_VERSION; }
@@ -1953,7 +1956,7 @@ int dqmc_last_pass_bytes(uint64_t *bytes, int max) {
     return k;
 }
 
-int dqmc_state_device(void **ptr, uint64_t *bytes) {
+int dqmc_bitmap_device(void **ptr, uint64_t *bytes) {
     if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
     const Plan p = make_plan(g_eng.state_n);
     if (ptr) *ptr = g_eng.state;
@@ -1961,7 +1964,7 @@ int dqmc_state_device(void **ptr, uint64_t *bytes) {
     return DQMC_OK;
 }
 
-int dqmc_state_download(void *host, uint64_t bytes) {
+int dqmc_bitmap_download(void *host, uint64_t bytes) {
     if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
     const Plan p = make_plan(g_eng.state_n);
     const uint64_t need = (uint64_t)p.nblocks * 32;

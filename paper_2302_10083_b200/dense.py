@@ -151,5 +151,5 @@ def prime_bitmap(tt: TruthTable) -> np.ndarray:
     _lib.check(rc)
     L.dqmc_free_result(ctypes.byref(res))
     out = np.zeros(state_bytes(n, 5) // 8, dtype=np.uint64)
-    _lib.check(L.dqmc_state_download(out.ctypes.data, out.nbytes))
+    _lib.check(L.dqmc_bitmap_download(out.ctypes.data, out.nbytes))
     return out
