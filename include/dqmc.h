@@ -137,6 +137,13 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
 int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, double p_on, double p_dc, uint64_t seed,
                            void *stream);
 
+/* Host conveniences for the CLI (f1): the frozen generator run on the device
+ * and copied to a host buffer of 2^n bytes; and the CLI listing order
+ * (wildcard count descending, rank ascending; cli.py:131-138) computed on the
+ * device (weight keys + stable radix sort) for `count` ascending ranks. */
+int dqmc_gen3_host(uint8_t *values_host, int n, double p_on, double p_dc, uint64_t seed);
+int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_t *out_host);
+
 /* Building blocks of the sharded multi-GPU path, all on
  * device buffers in the h = 5 layout (n >= 5):
  * dqmc_merge_device: complete MERGE of all n dimensions (no REDUCE) into

@@ -50,6 +50,8 @@ EXPORTS = (
     "dqmc_bitmap_download",
     "dqmc_gen3_device",
     "dqmc_gen3_range_device",
+    "dqmc_gen3_host",
+    "dqmc_order_by_weight",
     "dqmc_merge_device",
     "dqmc_reduce_extract_device",
     "dqmc_bitop_device",
@@ -134,6 +136,8 @@ def load() -> ctypes.CDLL:
             "dqmc_state_copy": (i32, [vp, ctypes.POINTER(ctypes.c_void_p)]),
             "dqmc_gen3_device": (i32, [vp, i32, dbl, dbl, u64, vp]),
             "dqmc_gen3_range_device": (i32, [vp, i64, i64, dbl, dbl, u64, vp]),
+            "dqmc_gen3_host": (i32, [vp, i32, dbl, dbl, u64]),
+            "dqmc_order_by_weight": (i32, [vp, i64, i32, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
             "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),
             "dqmc_bitop_device": (i32, [vp, vp, vp, u64, i32, vp]),

@@ -17,6 +17,7 @@
 //                          warp-aggregated popcount, decoupled look-back scan
 //                          and ordered compaction to int64 ranks.
 // Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -377,6 +378,23 @@ __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scr
         if (c < 0 || src < 0 || src + c > scap) continue;
         for (int i = lane; i < c; i += 32)
             if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
+    }
+}
+
+// wildcard count of every rank (ternary.py:139-146), stored as the sort key
+// n - weight so an ascending stable radix sort yields weight-descending order
+// with ranks ascending inside each weight (cli.py:134-135 ordering).
+__global__ void k_weight_keys(const int64_t *__restrict__ ranks, int64_t count, int n, uint8_t *__restrict__ keys) {
+    const int64_t stride = gridDim.x * (int64_t)blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+        uint64_t r = (uint64_t)ranks[i];
+        int w = 0;
+        for (int k = 0; k < n; k++) {
+            const uint64_t q = __umul64hi(r, 0xAAAAAAAAAAAAAAABull) >> 1;  // r / 3
+            w += (r - 3 * q) == 2;
+            r = q;
+        }
+        keys[i] = (uint8_t)(n - w);
     }
 }
 
@@ -1994,6 +2012,53 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
     int rc;
     if ((rc = validate(n, 0))) return rc;
     return dqmc_gen3_range_device(values_dev, 0, 1ll << n, p_on, p_dc, seed, stream);
+}
+
+int dqmc_gen3_host(uint8_t *values_host, int n, double p_on, double p_dc, uint64_t seed) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (!values_host) return set_err(DQMC_ERR_INVALID, "null output");
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_device())) return rc;
+        if ((rc = grow(g_eng.in_tmp, g_eng.in_tmp_cap, (size_t)1 << n, 1))) return rc;
+    }
+    if ((rc = dqmc_gen3_range_device((uint8_t *)g_eng.in_tmp, 0, 1ll << n, p_on, p_dc, seed, g_eng.stream))) return rc;
+    CK(cudaMemcpy(values_host, g_eng.in_tmp, (size_t)1 << n, cudaMemcpyDeviceToHost));
+    return DQMC_OK;
+}
+
+int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_t *out_host) {
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (count < 0 || (count && (!ranks_host || !out_host))) return set_err(DQMC_ERR_INVALID, "bad arguments");
+    if (count == 0) return DQMC_OK;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    cudaStream_t s = g_eng.stream;
+    int64_t *r_in = nullptr, *r_out = nullptr;
+    uint8_t *k_in = nullptr, *k_out = nullptr;
+    void *tmp = nullptr;
+    size_t tmpb = 0;
+    CK(cudaMalloc(&r_in, (size_t)count * 8));
+    CK(cudaMalloc(&r_out, (size_t)count * 8));
+    CK(cudaMalloc(&k_in, (size_t)count));
+    CK(cudaMalloc(&k_out, (size_t)count));
+    CK(cudaMemcpyAsync(r_in, ranks_host, (size_t)count * 8, cudaMemcpyHostToDevice, s));
+    const int grid = (int)std::min<int64_t>((count + 255) / 256, 148ll * 32);
+    k_weight_keys<<<grid, 256, 0, s>>>(r_in, count, n, k_in);
+    CK(cudaGetLastError());
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, k_in, k_out, r_in, r_out, (int)count, 0, 8, s));
+    CK(cudaMalloc(&tmp, tmpb));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmpb, k_in, k_out, r_in, r_out, (int)count, 0, 8, s));
+    CK(cudaMemcpyAsync(out_host, r_out, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(r_in);
+    cudaFree(r_out);
+    cudaFree(k_in);
+    cudaFree(k_out);
+    cudaFree(tmp);
+    return DQMC_OK;
 }
 
 int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state_out, void *stream) {
