@@ -174,3 +174,65 @@ def test_gpu_emulated_config4_k3(pkg, golden):
         want = pkg.prime_ranks_from_values(vd.cpu().numpy())
         raise AssertionError(_block_diff(got, want, 24, 3))
     assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()[:16] == g["ranks_sha256_prefix"]
+
+
+def _gpu_worker(rank, world, port, n, outdir):
+    """One rank of a 2-process run sharing cuda:0: real GPU block ops, host-staged
+    gloo exchange (no kernel waits on the other process)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2302_10083_b200 import _lib
+
+        k = world.bit_length() - 1
+        nl = n - k
+        vals = torch.empty(1 << nl, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().dqmc_gen3_range_device(vals.data_ptr(), rank << nl, 1 << nl, 0.75, 0.05, 3,
+                                                       torch.cuda.current_stream().cuda_stream))
+        parts = S.sharded_prime_ranks({rank: vals}, n, k, S.GpuOps(nl), S.DistComm(staging=True))
+        gathered = [None] * world if rank == 0 else None
+        dist.gather_object({t: v.cpu().numpy() for t, v in parts.items()}, gathered, dst=0)
+        if rank == 0:
+            allp = {}
+            for d in gathered:
+                allp.update(d)
+            np.save(os.path.join(outdir, "ranks.npy"), S.concat_ranks(allp))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,n", [(2, 18), (4, 19)])
+def test_gpu_multiprocess_sharded(world, n, tmp_path, pkg):
+    """The DistComm data path with GpuOps on real kernels, ranks as processes."""
+    from paper_2302_10083_b200 import device
+
+    mp.spawn(_gpu_worker, args=(world, _free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    got = np.load(tmp_path / "ranks.npy")
+    want = pkg.prime_ranks_from_values(device.gen3_device(n, 0.75, 0.05, 3).cpu().numpy())
+    assert np.array_equal(got, want), _block_diff(got, want, n, world.bit_length() - 1)
+
+
+@pytest.mark.gpu
+def test_bench_torchrun_two_ranks_gloo(tmp_path, pkg):
+    """bench.py under torch.distributed.run (N=2) through the sharded path, gloo
+    backend with host staging so both ranks can share this run's single GPU."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DQMC_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1", "--n", "18"]
+    r = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    from paper_2302_10083_b200 import device
+
+    want = len(pkg.prime_ranks_from_values(device.gen3_device(18, 0.75, 0.05, 3).cpu().numpy()))
+    assert line["n_gpus"] == 2 and line["config"]["primes"] == want and line["value"] > 0
+    assert line["scaling"] == "strong" and line["e2e"]["value"] > 0
