@@ -348,7 +348,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--nvars", dest="n", type=int, default=WORKLOAD["n"], help="variable count (default: config 4, n=24)")
     ap.add_argument("--cpu-sample-n", type=int, default=21)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

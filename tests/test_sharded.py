@@ -227,7 +227,7 @@ def test_bench_torchrun_two_ranks_gloo(tmp_path, pkg):
     env = dict(os.environ, DQMC_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1", "--n", "18"]
+           os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1", "--nvars", "18"]
     r = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
