@@ -199,12 +199,12 @@ def run_engine_bench(args):
     import paper_2302_10083_b200 as pkg
 
     rank, world, local = dist_info()
-    torch.cuda.set_device(local)
     n = args.n
     if world > 1:
         from paper_2302_10083_b200 import sharded
 
         return sharded.bench_main(args, WORKLOAD, METRIC, UNIT)
+    torch.cuda.set_device(local)
 
     dev = torch.device(f"cuda:{local}")
     values = device.gen3_device(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"], device=local)
