@@ -194,3 +194,41 @@ class TestFullSize:
         # and through the host API (same arrays)
         hr = pkg.prime_ranks_from_values(v.cpu().numpy())
         assert np.array_equal(hr, host)
+
+
+@pytest.mark.slow
+class TestLargestSingleGpu:
+    def test_n25_sampled(self, pkg, oracle_mod, gen_mod):
+        """n=25: 3^20 = 3.5e9 blocks (> 2^31) and a 111.6 GB state on one GPU.
+        No CPU reference fits, so: unique ascending int64 output, every sampled
+        prime is an implicant with no implicant one-widening parent, and every
+        sampled non-listed cube is not prime (independent checks, oracle.py:23-48)."""
+        from paper_2302_10083_b200 import device
+
+        n = 25
+        v = device.gen3_device(n, 0.75, 0.05, 3)
+        r, cnt = device.dense_prime_ranks_device(v, n)
+        host = r.cpu().numpy()
+        del r
+        assert cnt == len(host) and cnt > 0 and np.all(np.diff(host) > 0)
+        assert host[0] >= 0 and host[-1] < 3**n
+        on = v.cpu().numpy() != 0
+        rng = np.random.default_rng(25)
+        for r0 in rng.choice(host, 150, replace=False):
+            imp, mx = oracle_mod.is_prime_cube(int(r0), n, on)
+            assert imp and mx, int(r0)
+        # non-listed cubes: low-weight candidates near listed primes (the interesting ones)
+        listed = set(host.tolist())
+        checked = 0
+        for r0 in rng.choice(host, 400, replace=False):
+            s = oracle_mod.unrank(int(r0), n)
+            i = int(rng.integers(0, n))
+            for ch in "01*":
+                t = s[:i] + ch + s[i + 1 :]
+                rt = oracle_mod.rank(t)
+                if rt in listed or t.count("*") > 8:
+                    continue
+                imp, mx = oracle_mod.is_prime_cube(rt, n, on)
+                assert not (imp and mx), t
+                checked += 1
+        assert checked > 100
