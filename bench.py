@@ -218,18 +218,21 @@ def run_engine_bench(args):
         device.dense_prime_ranks_device(values, n, out=out)
     torch.cuda.synchronize()
 
-    # ---- value: device-resident, CUDA events on the launching stream (no per-pass timing)
+    # ---- value: device-resident, CUDA events on the launching stream (no per-pass
+    #      timing). Stream-ordered calls (DQMC_FLAG_ASYNC): the K steps queue back
+    #      to back, so a host-side stall cannot idle the GPU between steps.
     stream = torch.cuda.current_stream(dev)
+    cnt_dev = torch.zeros(args.steps, dtype=torch.int64, device=dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            _, c = device.dense_prime_ranks_device(values, n, out=out)
+        for i in range(args.steps):
+            device.enqueue_prime_ranks(values, n, out, cnt_dev[i : i + 1])
         ev1.record(stream)
         torch.cuda.synchronize()
-    assert c == cnt
+    assert cnt_dev.eq(cnt).all().item(), cnt_dev.tolist()
     t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
     value = 3**n / t_step
 
@@ -240,7 +243,9 @@ def run_engine_bench(args):
     for _ in range(args.steps):
         device.dense_prime_ranks_device(values, n, out=out, timing=True)
         tl = _lib.timings()
-        launches += len(tl) + 1  # + the uint8 -> bit packing kernel
+        # + the uint8 -> bit packing kernel and the async count publish (CUB's
+        # scan kernels inside the k_scan_tiles mark are library launches, not counted)
+        launches += len(tl) + 2
         for name, ms, by in tl:
             pass_times.setdefault(name, []).append(ms)
             pass_bytes[name] = by

@@ -55,6 +55,8 @@ extern "C" {
 #define DQMC_FLAG_KEEP_BITMAP 1u /* leave the final prime bitmap in the device state */
 #define DQMC_FLAG_TIMING 2u      /* record per-pass CUDA-event times (dqmc_last_timings) */
 #define DQMC_FLAG_COUNT_ONLY 4u  /* count primes, do not materialise ranks */
+#define DQMC_FLAG_ASYNC 8u       /* dqmc_primes_device only: stream-ordered, no host synchronisation,
+                                    CUDA-graph capturable; count_out is then a DEVICE int64 */
 
 /* input encodings */
 #define DQMC_IN_WORDS 0 /* TruthTable.words: max(1, 2^n/64) LE uint64, bit x = f(x) */
@@ -93,7 +95,16 @@ void dqmc_free_result(dqmc_result_t *res);
  * torch integration). ranks_dev may be NULL (count only). If the count
  * exceeds ranks_cap, *count_out is the true count and nothing beyond
  * ranks_cap is written (DQMC_ERR_RESOURCE is NOT raised; the caller grows
- * its buffer and calls again). Synchronises the stream to read the count. */
+ * its buffer and calls again). Synchronises the stream to read the count.
+ *
+ * With DQMC_FLAG_ASYNC nothing synchronises and nothing is allocated once an
+ * earlier synchronous call of the same n has sized the engine's buffers, so
+ * back-to-back calls queue on `stream` and the call can be captured into a
+ * CUDA graph. count_out is a device int64 written in stream order: the prime
+ * count if the ranks are complete, else -(count + 1) (ranks_cap or the
+ * engine's rank scratch was too small; call once synchronously, which grows
+ * the scratch). Concurrent async calls must share one stream (the engine's
+ * workspace is per process). */
 int dqmc_primes_device(const void *input_dev, int in_kind, int n, int64_t *ranks_dev, int64_t ranks_cap,
                        int64_t *count_out, uint32_t flags, void *stream);
 

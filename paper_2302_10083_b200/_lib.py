@@ -27,6 +27,7 @@ DQMC_ERR_NODEVICE = 4
 FLAG_KEEP_BITMAP = 1
 FLAG_TIMING = 2
 FLAG_COUNT_ONLY = 4
+FLAG_ASYNC = 8
 
 IN_WORDS = 0
 IN_U8 = 1

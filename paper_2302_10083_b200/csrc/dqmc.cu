@@ -41,10 +41,14 @@ using namespace dqmc;
 namespace {
 
 constexpr int kC0Max = 7;        // block axes in the contiguous tile (3^7 blocks = 68.3 KiB)
+constexpr int kC0MaxBlocks = 2187;  // 3^kC0Max
 constexpr int kGroupMax = 6;     // block axes per strided pass (3^6 rows x 128 B = 91 KiB)
 constexpr int kRowBlocks = 4;    // blocks per strided row (128 B)
 constexpr int kStridedThreads = 288;  // 9 warps: 27 sub-cube tasks per round divide evenly
 constexpr int kTileThreads = 224;  // 7 warps: the 4+3 C0 rounds divide into 1 and 3 tasks/thread
+// pass E: 12 warps x 3 CTAs (smem-limited) = 36 warps/SM to hide LDS/shuffle
+// latency; 56 registers/thread is the most that still fits 3 CTAs.
+constexpr int kFinalThreads = 384;
 
 enum Mode { MERGE_ONLY = 0, MERGE_REDUCE = 1, REDUCE_ONLY = 2 };
 
@@ -191,11 +195,12 @@ struct FinalArgs {
 // block range [b0, b1); lane l takes blocks b0+l, b0+l+32, ... for the
 // in-block axes and the popcount, then the same range word-by-word (lane =
 // word) for the ordered emission, which skips all-zero word groups.
+template <int NT>
 __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
-    constexpr int kMaxIter = 12;  // ceil(max warp range / 32): 3^7 blocks over 7 warps = 313 blocks
-    __shared__ int64_t s_warp_off[kTileThreads / 32];
+    constexpr int kMaxIter = ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;  // ceil(max warp range / 32)
+    __shared__ int64_t s_warp_off[NT / 32];
     __shared__ int64_t s_tile_off;
-    __shared__ uint8_t s_cnt[kTileThreads / 32][kMaxIter][32];  // block popcounts (<= 243)
+    __shared__ uint8_t s_cnt[NT / 32][kMaxIter][32];  // block popcounts (<= 243)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
@@ -205,42 +210,59 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     // (1) lane = block: in-block axes (if any left for this pass), kills, popcount
     //     (loops kept rolled: the kernel must stay inside the instruction cache)
     int cnt = 0;
+    const bool plain = !fa.ib_mask && !fa.kill && !fa.bitmap_out;
+    if (plain) {  // count only: word order within the block does not matter
 #pragma unroll 1
-    for (int j = 0; j < nj; j++) {
-        int cj = 0;
-        {
+        for (int j = 0; j < nj; j++) {
             const int b = b0 + 32 * j + lane;
+            int cj = 0;
             if (b < b1) {
-                uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
-                const uint4 ya = p[h], yb = p[h ^ 1];
-                uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
-                if (fa.ib_mask) {
-                    uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                    inblock_reduce(v, fa.ib_mask);
-                    x0 = make_uint4(v[0], v[1], v[2], v[3]);
-                    x1 = make_uint4(v[4], v[5], v[6], v[7]);
-                }
-                if (fa.kill) {
-                    const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill + (blk0 + b) * 8);
-                    const uint4 k0 = kq[0], k1 = kq[1];
-                    x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
-                    x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
-                }
-                if (fa.ib_mask || fa.kill) {
-                    p[h] = h ? x1 : x0;
-                    p[h ^ 1] = h ? x0 : x1;
-                }
-                if (fa.bitmap_out) {
-                    uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
-                    q[0] = x0;
-                    q[1] = x1;
-                }
+                const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+                const uint4 x0 = p[h], x1 = p[h ^ 1];
                 cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
                      __popc(x1.z) + __popc(x1.w);
                 cnt += cj;
             }
+            s_cnt[warp][j][lane] = (uint8_t)cj;
         }
-        s_cnt[warp][j][lane] = (uint8_t)cj;
+    } else {
+#pragma unroll 1
+        for (int j = 0; j < nj; j++) {
+            int cj = 0;
+            {
+                const int b = b0 + 32 * j + lane;
+                if (b < b1) {
+                    uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+                    const uint4 ya = p[h], yb = p[h ^ 1];
+                    uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                    if (fa.ib_mask) {
+                        uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                        inblock_reduce(v, fa.ib_mask);
+                        x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                        x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                    }
+                    if (fa.kill) {
+                        const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill + (blk0 + b) * 8);
+                        const uint4 k0 = kq[0], k1 = kq[1];
+                        x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
+                        x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
+                    }
+                    if (fa.ib_mask || fa.kill) {
+                        p[h] = h ? x1 : x0;
+                        p[h ^ 1] = h ? x0 : x1;
+                    }
+                    if (fa.bitmap_out) {
+                        uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+                        q[0] = x0;
+                        q[1] = x1;
+                    }
+                    cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
+                         __popc(x1.z) + __popc(x1.w);
+                    cnt += cj;
+                }
+            }
+            s_cnt[warp][j][lane] = (uint8_t)cj;
+        }
     }
     int wsum = cnt;
 #pragma unroll
@@ -362,6 +384,13 @@ __global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__r
 
 // Copy every tile's ranks from its scratch range to its rank-order position
 // (one warp per tile, coalesced 8-B copies).
+// DQMC_FLAG_ASYNC: publish the count in stream order; -(count + 1) flags an
+// incomplete rank list (output or scratch too small).
+__global__ void k_publish_count(const int64_t *__restrict__ total, int64_t limit, int64_t *__restrict__ dst) {
+    const int64_t t = *total;
+    *dst = t <= limit ? t : -(t + 1);
+}
+
 __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
                                                  const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
                                                  int64_t *__restrict__ out, int64_t cap, int64_t ntiles,
@@ -525,7 +554,7 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__res
 // pass E: one CTA per C0 tile (3^G blocks), tiles taken in rank order by
 // ticket; the tile arrives in shared memory with one TMA bulk copy.
 template <int G>
-__global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa) {
+__global__ void __launch_bounds__(kFinalThreads, 3) k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa) {
     extern __shared__ __align__(128) uint32_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     constexpr int NB = pow3i(G);
@@ -539,7 +568,7 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_final(const uint32_t *__res
     __syncthreads();
     mbar_wait(&mbar, 0);
     tile_reduce_c0_t<G, 0>(sm);
-    tile_finish(sm, NB, tile, blk0, fa);
+    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa);
 }
 
 // n <= 12: the whole problem is one tile; one CTA does A and E.
@@ -547,7 +576,7 @@ __global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restri
     extern __shared__ __align__(16) uint32_t sm[];
     tile_build(sm, tt32, g, 0);
     tile_reduce_c0(sm, g);
-    tile_finish(sm, (int)pow3l(g), 0, 0, fa);
+    tile_finish<kTileThreads>(sm, (int)pow3l(g), 0, 0, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -1437,7 +1466,7 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
     switch (g) {
 #define CASE(G)                                                                         \
     case G:                                                                             \
-        k_c0_final<G><<<(unsigned)ntiles, kTileThreads, smem, s>>>(state, fa);          \
+        k_c0_final<G><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa);          \
         break;
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
@@ -1451,7 +1480,7 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
 // A+E, when tt32 != null) or a merged/reduced state. Returns the prime count.
 int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const uint32_t *kill, uint32_t ib_mask,
               int64_t rank_add, int64_t *ranks, int64_t cap, bool count_only, uint32_t *bitmap_out, int64_t *count,
-              Timer &tm, cudaStream_t s) {
+              Timer &tm, cudaStream_t s, int64_t *count_dev = nullptr) {
     const uint64_t S = (uint64_t)p.nblocks * 32;
     const int64_t ntiles = p.T == 0 ? 1 : pow3l(p.T);
     const int tile_smem = (int)pow3l(p.g) * 32;
@@ -1505,6 +1534,12 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
                                        ntiles, (int64_t)g_eng.scratch_cap);
         CK(cudaGetLastError());
         tm.mark("k_reorder", (uint64_t)ntiles * 16);
+    }
+    if (count_dev) {  // DQMC_FLAG_ASYNC: no host synchronisation
+        const int64_t limit = count_only ? INT64_MAX : (direct ? cap : std::min<int64_t>(cap, (int64_t)g_eng.scratch_cap));
+        k_publish_count<<<1, 1, 0, s>>>(g_eng.total, limit, count_dev);
+        CK(cudaGetLastError());
+        return DQMC_OK;
     }
     int64_t total = 0;
     CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1581,10 +1616,12 @@ void add_rank_bytes(Timer &tm, int64_t written) {
 // merged state it reads; with a bitmap output it rewrites the same P).
 int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, const uint32_t *kill,
                     uint32_t ib_mask, int64_t rank_add, int64_t *ranks, int64_t cap, bool count_only,
-                    uint32_t *bitmap_out, int64_t *count, Timer &tm, cudaStream_t s) {
+                    uint32_t *bitmap_out, int64_t *count, Timer &tm, cudaStream_t s, int64_t *count_dev = nullptr) {
     int rc;
-    if ((rc = run_final(p, tt32, state, kill, ib_mask, rank_add, ranks, cap, count_only, bitmap_out, count, tm, s)))
+    if ((rc = run_final(p, tt32, state, kill, ib_mask, rank_add, ranks, cap, count_only, bitmap_out, count, tm, s,
+                        count_dev)))
         return rc;
+    if (count_dev) return DQMC_OK;  // async: the caller sees -(count + 1) and retries synchronously
     const bool direct = (p.T == 0);
     if (!count_only && !direct && (size_t)*count > g_eng.scratch_cap) {
         g_eng.scratch_want = (size_t)((double)*count * 1.05) + 1024;
@@ -1601,7 +1638,8 @@ int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, 
 // Run the whole single-GPU plan on a device-resident 32-bit truth table.
 int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, int64_t *count, uint32_t flags,
              cudaStream_t s) {
-    Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
+    int64_t *count_dev = (flags & DQMC_FLAG_ASYNC) ? count : nullptr;  // async: count is a device pointer
+    Timer tm{(flags & DQMC_FLAG_TIMING) != 0 && !count_dev, s};
     const bool keep = (flags & DQMC_FLAG_KEEP_BITMAP) != 0;
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0 || ranks == nullptr;
     int rc;
@@ -1615,15 +1653,15 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
         if ((rc = run_merge(p, tt32, g_eng.state, false, tm, s))) return rc;
         if ((rc = run_reduce(p, g_eng.state, true, tm, s))) return rc;
         if ((rc = run_final_retry(p, nullptr, g_eng.state, nullptr, p.ib_E, -p.rank_sub, ranks, cap, count_only,
-                                  keep ? g_eng.state : nullptr, &total, tm, s)))
+                                  keep ? g_eng.state : nullptr, &total, tm, s, count_dev)))
             return rc;
     } else {
         if ((rc = run_final_retry(p, tt32, nullptr, nullptr, p.ib_E, -p.rank_sub, ranks, cap, count_only,
-                                  keep ? g_eng.state : nullptr, &total, tm, s)))
+                                  keep ? g_eng.state : nullptr, &total, tm, s, count_dev)))
             return rc;
     }
     tm.finish();
-    *count = total;
+    if (!count_dev) *count = total;
     g_eng.state_n = keep ? p.n : -1;
     return DQMC_OK;
 }

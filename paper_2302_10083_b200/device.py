@@ -53,3 +53,61 @@ def dense_prime_ranks_device(
             L.dqmc_primes_device(table.data_ptr(), kind, n, out.data_ptr(), out.numel(), ctypes.byref(cnt), flags, stream)
         )
     return out[: cnt.value], int(cnt.value)
+
+
+def _kind(table: torch.Tensor) -> int:
+    if not table.is_cuda:
+        raise ValueError("table must be a CUDA tensor")
+    if table.dtype == torch.uint8:
+        return _lib.IN_U8
+    if table.dtype not in (torch.int64, torch.uint64):
+        raise ValueError("word tables must be int64/uint64")
+    return _lib.IN_WORDS
+
+
+def enqueue_prime_ranks(table: torch.Tensor, n: int, out: torch.Tensor, count: torch.Tensor) -> None:
+    """Stream-ordered call (DQMC_FLAG_ASYNC): nothing synchronises, so calls
+    queue back to back and can be captured into a CUDA graph. ``count`` (int64
+    cuda, one element) receives the prime count, or -(count + 1) if ``out`` or
+    the engine's rank scratch was too small (call dense_prime_ranks_device once
+    first: it sizes the scratch for this n)."""
+    if count.dtype != torch.int64 or not count.is_cuda or count.numel() < 1:
+        raise ValueError("count must be a one-element int64 CUDA tensor")
+    if out.dtype != torch.int64 or not out.is_cuda:
+        raise ValueError("out must be an int64 CUDA tensor")
+    stream = torch.cuda.current_stream(table.device).cuda_stream
+    _lib.check(_lib.load().dqmc_primes_device(table.data_ptr(), _kind(table), n, out.data_ptr(), out.numel(),
+                                              ctypes.cast(count.data_ptr(), ctypes.POINTER(ctypes.c_int64)),
+                                              _lib.FLAG_ASYNC, stream))
+
+
+class PrimesGraph:
+    """One prime-implicant call on fixed device buffers, captured once as a
+    CUDA graph and replayed (no per-call host work beyond one graph launch).
+    ``table`` may be refilled in place between replays; ``ranks()`` reads the
+    result of the last replay (synchronising)."""
+
+    def __init__(self, table: torch.Tensor, n: int, headroom: float = 1.05):
+        self.table, self.n = table, n
+        r, cnt = dense_prime_ranks_device(table, n)  # sizes the engine's workspace for n
+        del r
+        self.out = torch.empty(int(cnt * headroom) + 1024, dtype=torch.int64, device=table.device)
+        self.count = torch.zeros(1, dtype=torch.int64, device=table.device)
+        s = torch.cuda.Stream(table.device)
+        s.wait_stream(torch.cuda.current_stream(table.device))
+        with torch.cuda.stream(s):
+            enqueue_prime_ranks(table, n, self.out, self.count)  # warm-up on the capture stream
+        torch.cuda.current_stream(table.device).wait_stream(s)
+        torch.cuda.synchronize(table.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=s):
+            enqueue_prime_ranks(table, n, self.out, self.count)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def ranks(self) -> torch.Tensor:
+        c = int(self.count.item())
+        if c < 0:
+            raise RuntimeError(f"graph output too small for {-c - 1} primes; rebuild the PrimesGraph")
+        return self.out[:c]

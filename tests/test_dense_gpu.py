@@ -232,3 +232,60 @@ class TestLargestSingleGpu:
                 assert not (imp and mx), t
                 checked += 1
         assert checked > 100
+
+
+class TestAsyncAndGraph:
+    """DQMC_FLAG_ASYNC (stream-ordered, no host sync) and CUDA-graph replay
+    give the synchronous results bit for bit."""
+
+    def test_async_matches_sync(self, pkg):
+        import torch
+        from paper_2302_10083_b200 import device
+
+        for n, dtype in ((14, "u8"), (18, "u8"), (16, "words")):
+            v = device.gen3_device(n, 0.6, 0.1, n)
+            if dtype == "words":
+                v = (v.view(-1, 8).ne(0).to(torch.int64) << torch.arange(8, device=v.device)).sum(1).to(torch.uint8)
+                v = v.view(torch.int64) if v.numel() >= 8 else v
+            ref, cnt = device.dense_prime_ranks_device(v, n)
+            ref = ref.clone()
+            out = torch.full((cnt + 100,), -7, dtype=torch.int64, device="cuda")
+            c = torch.zeros(1, dtype=torch.int64, device="cuda")
+            for _ in range(3):  # back-to-back, no host sync in between
+                device.enqueue_prime_ranks(v, n, out, c)
+            assert int(c.item()) == cnt
+            assert torch.equal(out[:cnt], ref)
+
+    def test_async_flags_short_output(self, pkg):
+        import torch
+        from paper_2302_10083_b200 import device
+
+        v = device.gen3_device(16, 0.7, 0.0, 2)
+        _, cnt = device.dense_prime_ranks_device(v, 16)
+        out = torch.empty(cnt - 1, dtype=torch.int64, device="cuda")
+        c = torch.zeros(1, dtype=torch.int64, device="cuda")
+        device.enqueue_prime_ranks(v, 16, out, c)
+        assert int(c.item()) == -(cnt + 1)
+
+    def test_graph_replay_and_refill(self, pkg):
+        import torch
+        from paper_2302_10083_b200 import _lib, device
+
+        n = 20
+        v = device.gen3_device(n, 0.75, 0.05, 3)
+        g = device.PrimesGraph(v, n)
+        for _ in range(2):
+            g.replay()
+        ref, cnt = device.dense_prime_ranks_device(v, n)
+        assert torch.equal(g.ranks(), ref)
+        # refill the captured input in place with another function, replay
+        _lib.check(_lib.load().dqmc_gen3_device(v.data_ptr(), n, 0.7, 0.05, 9,
+                                                torch.cuda.current_stream().cuda_stream))
+        g.replay()
+        ref2, cnt2 = device.dense_prime_ranks_device(v, n)
+        assert cnt2 != cnt
+        if cnt2 <= g.out.numel():
+            assert torch.equal(g.ranks(), ref2)
+        else:
+            with pytest.raises(RuntimeError):
+                g.ranks()
