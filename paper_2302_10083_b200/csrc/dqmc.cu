@@ -189,88 +189,111 @@ struct FinalArgs {
 };
 
 
-// In-block reduce, popcount, decoupled look-back and ordered compaction of one
-// tile (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order
-// is rank order, so the output needs no sort). Warp w owns the contiguous
-// block range [b0, b1); lane l takes blocks b0+l, b0+l+32, ... for the
-// in-block axes and the popcount, then the same range word-by-word (lane =
-// word) for the ordered emission, which skips all-zero word groups.
+// In-block reduce, popcount and ordered compaction of one tile
+// (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order is
+// rank order, so the output needs no sort). Warp w owns the contiguous block
+// range [b0, b1); lane l takes blocks b0+l, b0+l+32, ... (group j = the j-th
+// 32 blocks). Block counts stay in registers, two 16-bit fields per word, so
+// one packed warp scan serves every group: the phases are short latency
+// chains, which is what bounds this pass (3 CTAs/SM, smem-limited).
 template <int NT>
 __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
     constexpr int kMaxIter = ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;  // ceil(max warp range / 32)
+    constexpr int kPk = (kMaxIter + 1) / 2;
     __shared__ int64_t s_warp_off[NT / 32];
     __shared__ int64_t s_tile_off;
-    __shared__ uint8_t s_cnt[NT / 32][kMaxIter][32];  // block popcounts (<= 243)
+    __shared__ uint8_t s_cnt[NT / 32][kMaxIter][32];  // slow path only: block popcounts (<= 243)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
-    const int nj = (b1 - b0 + 31) >> 5;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
 
-    // (1) lane = block: in-block axes (if any left for this pass), kills, popcount
-    //     (loops kept rolled: the kernel must stay inside the instruction cache)
-    int cnt = 0;
-    const bool plain = !fa.ib_mask && !fa.kill && !fa.bitmap_out;
-    if (plain) {  // count only: word order within the block does not matter
-#pragma unroll 1
-        for (int j = 0; j < nj; j++) {
+    // (1) lane = block: popcount (+ in-block axes, kills, bitmap on the slow path)
+    uint32_t pk[kPk];
+#pragma unroll
+    for (int i = 0; i < kPk; i++) pk[i] = 0;
+    if (!fa.ib_mask && !fa.kill && !fa.bitmap_out) {  // count only: word order does not matter
+#pragma unroll
+        for (int j = 0; j < kMaxIter; j++) {
             const int b = b0 + 32 * j + lane;
-            int cj = 0;
             if (b < b1) {
                 const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
                 const uint4 x0 = p[h], x1 = p[h ^ 1];
-                cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
-                     __popc(x1.z) + __popc(x1.w);
-                cnt += cj;
+                const uint32_t cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) +
+                                    __popc(x1.y) + __popc(x1.z) + __popc(x1.w);
+                pk[j >> 1] |= cj << (16 * (j & 1));
             }
-            s_cnt[warp][j][lane] = (uint8_t)cj;
         }
     } else {
+        // rolled (the in-block code is large: the kernel must stay inside the instruction cache)
 #pragma unroll 1
-        for (int j = 0; j < nj; j++) {
+        for (int j = 0; j < kMaxIter; j++) {
+            const int b = b0 + 32 * j + lane;
             int cj = 0;
-            {
-                const int b = b0 + 32 * j + lane;
-                if (b < b1) {
-                    uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
-                    const uint4 ya = p[h], yb = p[h ^ 1];
-                    uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
-                    if (fa.ib_mask) {
-                        uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                        inblock_reduce(v, fa.ib_mask);
-                        x0 = make_uint4(v[0], v[1], v[2], v[3]);
-                        x1 = make_uint4(v[4], v[5], v[6], v[7]);
-                    }
-                    if (fa.kill) {
-                        const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill + (blk0 + b) * 8);
-                        const uint4 k0 = kq[0], k1 = kq[1];
-                        x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
-                        x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
-                    }
-                    if (fa.ib_mask || fa.kill) {
-                        p[h] = h ? x1 : x0;
-                        p[h ^ 1] = h ? x0 : x1;
-                    }
-                    if (fa.bitmap_out) {
-                        uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
-                        q[0] = x0;
-                        q[1] = x1;
-                    }
-                    cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
-                         __popc(x1.z) + __popc(x1.w);
-                    cnt += cj;
+            if (b < b1) {
+                uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                if (fa.ib_mask) {
+                    uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    inblock_reduce(v, fa.ib_mask);
+                    x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                    x1 = make_uint4(v[4], v[5], v[6], v[7]);
                 }
+                if (fa.kill) {
+                    const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill + (blk0 + b) * 8);
+                    const uint4 k0 = kq[0], k1 = kq[1];
+                    x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
+                    x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
+                }
+                if (fa.ib_mask || fa.kill) {
+                    p[h] = h ? x1 : x0;
+                    p[h ^ 1] = h ? x0 : x1;
+                }
+                if (fa.bitmap_out) {
+                    uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+                    q[0] = x0;
+                    q[1] = x1;
+                }
+                cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
+                     __popc(x1.z) + __popc(x1.w);
             }
             s_cnt[warp][j][lane] = (uint8_t)cj;
         }
-    }
-    int wsum = cnt;
+        __syncwarp();
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        for (int j = 0; j < kMaxIter; j++) pk[j >> 1] |= (uint32_t)s_cnt[warp][j][lane] << (16 * (j & 1));
+    }
+
+    // (2) packed inclusive warp scan (fields <= 32 * 243 < 2^16: no carries
+    //     between fields), group bases, the warp's total
+    uint32_t inc[kPk];
+#pragma unroll
+    for (int i = 0; i < kPk; i++) inc[i] = pk[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < kPk; i++) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc[i], o);
+            if (lane >= o) inc[i] += y;
+        }
+    }
+    int gbase[kMaxIter];
+    int wsum = 0;
+#pragma unroll
+    for (int i = 0; i < kPk; i++) {
+        const uint32_t t = __shfl_sync(0xffffffffu, inc[i], 31);
+        gbase[2 * i] = wsum;
+        wsum += (int)(t & 0xffffu);
+        if (2 * i + 1 < kMaxIter) {
+            gbase[2 * i + 1] = wsum;
+            wsum += (int)(t >> 16);
+        }
+    }
     if (lane == 0) s_warp_off[warp] = wsum;
     __syncthreads();
 
-    // (2) reserve this tile's range in the scratch output with one atomic (no
+    // (3) reserve this tile's range in the scratch output with one atomic (no
     //     waiting on other tiles); k_scan_tiles + k_reorder restore rank order.
     if (threadIdx.x == 0) {
         int64_t acc = 0;
@@ -287,53 +310,28 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     __syncthreads();
     if (fa.out == nullptr) return;
 
-    // (3) ordered emission within the tile. Per 32-block group: warp scan of
-    //     the block counts from (1), then a load-balanced walk: lane q of each
-    //     step finds the block holding output q (binary search over the scan
-    //     by shuffles) and that block's (q - excl)-th set bit, so every warp
-    //     store writes 32 consecutive ranks.
-    int64_t off = s_tile_off + s_warp_off[warp];
-#pragma unroll 1
-    for (int j = 0; j < nj; j++) {
-        {
-            const int c = s_cnt[warp][j][lane];
-            if (__ballot_sync(0xffffffffu, c != 0) != 0u) {
-                int incl = c;
+    // (4) ordered emission: every lane with a nonzero block writes its ranks at
+    //     off + group base + exclusive count (ascending by lane: the stores of
+    //     one step coalesce). Primes are sparse (~0.2 per block at n = 24).
+    const int64_t off = s_tile_off + s_warp_off[warp];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int excl = incl - c;
-                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                const int gb = b0 + 32 * j;  // first block of the group
-                for (int q0 = 0; q0 < total; q0 += 32) {
-                    const int q = q0 + lane;
-                    int L = 0;
+    for (int j = 0; j < kMaxIter; j++) {
+        const uint32_t c = (pk[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        if (c) {
+            const int b = b0 + 32 * j + lane;
+            const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+            const uint4 x0 = p[0], x1 = p[1];
+            const uint32_t wv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            int64_t pos = off + gbase[j] + (int)(((inc[j >> 1] >> (16 * (j & 1))) & 0xffffu) - c);
+            const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
 #pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int ex = __shfl_sync(0xffffffffu, excl, L + step);
-                        if (ex <= q) L += step;
-                    }
-                    const int exL = __shfl_sync(0xffffffffu, excl, L);
-                    if (q < total) {
-                        int r = q - exL;
-                        const int blk = gb + L;
-                        const uint32_t *wp = sm + blk * 8;
-                        int k = 0;
-                        uint32_t w = wp[0];
-                        int pc = __popc(w);
-                        while (r >= pc) {
-                            r -= pc;
-                            w = wp[++k];
-                            pc = __popc(w);
-                        }
-                        for (int t = 0; t < r; t++) w &= w - 1;
-                        const int64_t pos = off + q;
-                        if (pos < fa.cap) fa.out[pos] = (blk0 + blk) * 243 + k * 32 + (__ffs(w) - 1) + fa.rank_add;
-                    }
+            for (int k = 0; k < 8; k++) {
+                uint32_t w = wv[k];
+                while (w) {
+                    if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                    pos++;
+                    w &= w - 1;
                 }
-                off += total;
             }
         }
     }
