@@ -754,6 +754,8 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
@@ -807,7 +809,10 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t full[2], computed[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // items strided over the grid: the CTAs work on adjacent columns at the same
+    // time (a contiguous range per CTA measured 16.0 vs 13.9 ms at n = 24)
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto item = [&](int64_t i) { return blockIdx.x + i * gridDim.x; };
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
@@ -823,33 +828,47 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             for (int64_t i = 0; i < L + 2; i++) {
                 const int b = (int)(i & 1);
                 uint32_t *tile = smem + b * SM::TILE_WORDS;
-                if (i >= 2) {
-                    const int64_t it = blockIdx.x + (i - 2) * gridDim.x;
+                const bool st = i >= 2;
+                if (st) {
+                    const int64_t it = item(i - 2);
                     mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
                     const int c0 = (int)((it % ncol) * 32), c2 = (int)(it / ncol);
 #pragma unroll
-                    for (int x = 0; x < SM::NBOX; x++)
+                    for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
                         tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile + x * SM::BOXR * 32);
-                    bulk_commit();
-                    bulk_wait_read0();
+                        bulk_commit();
+                    }
                 }
                 if (i < L) {
-                    const int64_t it = blockIdx.x + i * gridDim.x;
+                    const int64_t it = item(i);
                     const int c0 = (int)((it % ncol) * 32), outer = (int)(it / ncol);
                     if (MODE == REDUCE_ONLY) {
+                        // each box is reloaded as soon as its store has read it out of
+                        // smem: the next tile's load overlaps the previous tile's store
                         mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
+                        static_assert(SM::NBOX <= 3, "box-wise store/load overlap handles <= 3 boxes");
 #pragma unroll
-                        for (int x = 0; x < SM::NBOX; x++)
+                        for (int x = 0; x < SM::NBOX; x++) {
+                            if (st) {
+                                if (SM::NBOX - 1 - x == 2) bulk_wait_read<2>();
+                                else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
+                                else bulk_wait_read<0>();
+                            }
                             tma_load_3d(tile + x * SM::BOXR * 32, &tmap, c0, x * SM::BOXR, outer, &full[b]);
+                        }
                     } else {
-                        // binary rows: one 5-D box {32 words, 2, .., 2} per binary rho2
-                        uint32_t *st = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
+                        // binary rows: one 5-D box {32 words, 2, .., 2} per binary rho2; the
+                        // compute warps rewrite tile b once these land, so the store of the
+                        // previous tile in b must have read it out first
+                        if (st) bulk_wait_read<0>();
+                        uint32_t *stg = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
                         mbar_expect_tx(&full[b], SM::STAGE_WORDS * 4);
 #pragma unroll
                         for (int b2 = 0; b2 < B2; b2++)
-                            tma_load_5d(st + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
+                            tma_load_5d(stg + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
                     }
                 }
+                if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
             }
             bulk_wait0();
         }
