@@ -202,7 +202,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     constexpr int kPk = (kMaxIter + 1) / 2;
     __shared__ int64_t s_warp_off[NT / 32];
     __shared__ int64_t s_tile_off;
-    __shared__ uint8_t s_cnt[NT / 32][kMaxIter][32];  // slow path only: block popcounts (<= 243)
+    __shared__ uint16_t s_cnt[NT / 32][kMaxIter][32];  // slow-path block popcounts, then the emission list
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
@@ -258,7 +258,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                 cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
                      __popc(x1.z) + __popc(x1.w);
             }
-            s_cnt[warp][j][lane] = (uint8_t)cj;
+            s_cnt[warp][j][lane] = (uint16_t)cj;
         }
         __syncwarp();
 #pragma unroll
@@ -310,28 +310,55 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     __syncthreads();
     if (fa.out == nullptr) return;
 
-    // (4) ordered emission: every lane with a nonzero block writes its ranks at
-    //     off + group base + exclusive count (ascending by lane: the stores of
-    //     one step coalesce). Primes are sparse (~0.2 per block at n = 24).
+    // (4) ordered emission. Primes are sparse (~0.2 per block at n = 24, ~5
+    //     nonzero blocks per 32-block group), so the nonzero blocks of the
+    //     warp's range are first compacted into a list (ballot + prefix;
+    //     s_cnt is free again), then processed 32 at a time with every lane
+    //     busy: reload the block, popcount, one warp scan for the positions,
+    //     walk the set bits. Stores of one step ascend with the lane and coalesce.
     const int64_t off = s_tile_off + s_warp_off[warp];
+    uint16_t *lst = &s_cnt[warp][0][0];  // kMaxIter * 32 entries >= the warp's range
+    const uint32_t lt = (1u << lane) - 1u;
+    int n = 0;
 #pragma unroll
     for (int j = 0; j < kMaxIter; j++) {
         const uint32_t c = (pk[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-        if (c) {
-            const int b = b0 + 32 * j + lane;
+        const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
+        if (c) lst[n + __popc(m & lt)] = (uint16_t)(32 * j + lane);
+        n += __popc(m);
+    }
+    __syncwarp();
+    int64_t run = off;
+#pragma unroll 1
+    for (int e0 = 0; e0 < n; e0 += 32) {
+        const int e = e0 + lane;
+        uint32_t wv[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        int cnt = 0, b = 0;
+        if (e < n) {
+            b = b0 + lst[e];
             const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
             const uint4 x0 = p[0], x1 = p[1];
-            const uint32_t wv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            int64_t pos = off + gbase[j] + (int)(((inc[j >> 1] >> (16 * (j & 1))) & 0xffffu) - c);
-            const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+            wv[0] = x0.x, wv[1] = x0.y, wv[2] = x0.z, wv[3] = x0.w;
+            wv[4] = x1.x, wv[5] = x1.y, wv[6] = x1.z, wv[7] = x1.w;
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                uint32_t w = wv[k];
-                while (w) {
-                    if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
-                    pos++;
-                    w &= w - 1;
-                }
+            for (int k = 0; k < 8; k++) cnt += __popc(wv[k]);
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int64_t pos = run + (incl - cnt);
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t w = wv[k];
+            while (w) {
+                if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                pos++;
+                w &= w - 1;
             }
         }
     }
