@@ -147,12 +147,17 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
 /* Points [x0, x0 + count) only (a rank's slice of a sharded table). */
 int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, double p_on, double p_dc, uint64_t seed,
                            void *stream);
+/* BASELINE config 3 (n = 20): P = stable argsort of the
+ * generator values of points 0..1023 under `seed` (a bijection on 10 bits);
+ * v[x | P(x) << 10] = 0 for every x, all other 2^20 points 1. */
+int dqmc_gen_sbox_device(uint8_t *values_dev, uint64_t seed, void *stream);
 
 /* Host conveniences for the CLI (f1): the frozen generator run on the device
  * and copied to a host buffer of 2^n bytes; and the CLI listing order
  * (wildcard count descending, rank ascending; cli.py:131-138) computed on the
  * device (weight keys + stable radix sort) for `count` ascending ranks. */
 int dqmc_gen3_host(uint8_t *values_host, int n, double p_on, double p_dc, uint64_t seed);
+int dqmc_gen_sbox_host(uint8_t *values_host, uint64_t seed); /* 2^20 bytes */
 int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_t *out_host);
 
 /* Building blocks of the sharded multi-GPU path, all on

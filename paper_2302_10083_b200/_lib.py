@@ -52,6 +52,8 @@ EXPORTS = (
     "dqmc_gen3_device",
     "dqmc_gen3_range_device",
     "dqmc_gen3_host",
+    "dqmc_gen_sbox_device",
+    "dqmc_gen_sbox_host",
     "dqmc_order_by_weight",
     "dqmc_merge_device",
     "dqmc_reduce_extract_device",
@@ -138,6 +140,8 @@ def load() -> ctypes.CDLL:
             "dqmc_gen3_device": (i32, [vp, i32, dbl, dbl, u64, vp]),
             "dqmc_gen3_range_device": (i32, [vp, i64, i64, dbl, dbl, u64, vp]),
             "dqmc_gen3_host": (i32, [vp, i32, dbl, dbl, u64]),
+            "dqmc_gen_sbox_device": (i32, [vp, u64, vp]),
+            "dqmc_gen_sbox_host": (i32, [vp, u64]),
             "dqmc_order_by_weight": (i32, [vp, i64, i32, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
             "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),

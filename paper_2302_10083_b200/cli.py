@@ -16,7 +16,8 @@ Mirrors the dense-path subset of the reference CLI
 Inputs: --input PATH in the 'bits' text format (one '0'/'1' per point, index 0
 first, whitespace ignored; ttio.py format "bits") or generated on the device
 from --n/--density/--seed with the reference's frozen generator (ttio.py:331-378),
-optionally with --dc (three-valued table, don't-care = on).
+optionally with --dc (three-valued table, don't-care = on), or
+--config K for a BASELINE.json workload (configs.py).
 Other text formats (hex/minterms/pla) are out of scope.
 
 Exit codes (cli.py:320-333): 0 success, 1 bad input or usage, 2 resource
@@ -93,8 +94,13 @@ def _input(args):
         with open(args.input) if args.input != "-" else sys.stdin as fh:
             tt = read_bits(fh.read())
         return tt.n, tt, None
+    if args.config is not None:
+        from .configs import CONFIGS, config_values_host
+
+        v = config_values_host(args.config, args.n)
+        return (args.n or CONFIGS[args.config]["n"]), None, v
     if args.n is None or args.density is None:
-        raise ParseError("provide --input PATH, or both --n and --density to generate")
+        raise ParseError("provide --input PATH, --config K, or both --n and --density to generate")
     v = generate_values(args.n, args.density, args.seed, args.dc)
     return args.n, None, v
 
@@ -195,6 +201,7 @@ def _add_common(p):
     g.add_argument("--density", type=float, help="P(on) for generated input")
     g.add_argument("--dc", type=float, default=0.0, help="P(don't care) for generated input (counted as on)")
     g.add_argument("--seed", type=int, default=0)
+    g.add_argument("--config", type=int, choices=(1, 2, 3, 4, 5), help="BASELINE.json workload (--n overrides its size)")
     e = p.add_argument_group("engine")
     e.add_argument("--h", type=int, help="dense split, validated as the reference (result independent of it)")
     e.add_argument("--unroll", choices=("on", "off"), default="on")

@@ -123,6 +123,26 @@ __global__ void k_gen3(uint8_t *__restrict__ out, int64_t x0, int64_t npts, uint
     }
 }
 
+// config 3 S-box table: one CTA of 1024 threads ranks the 1024 generator
+// values (stable: ties by index), P[rank(i)] = i, then clears v[x | P(x) << 10]
+// (the table was set to 1 beforehand).
+__global__ void __launch_bounds__(1024) k_sbox(uint8_t *__restrict__ v, uint64_t seed) {
+    __shared__ uint64_t val[1024];
+    __shared__ uint16_t perm[1024];
+    const int i = threadIdx.x;
+    val[i] = mix64(seed + ((uint64_t)i + 1) * 0x9E3779B97F4A7C15ull);
+    __syncthreads();
+    const uint64_t me = val[i];
+    int rank = 0;
+    for (int j = 0; j < 1024; j++) {
+        const uint64_t o = val[j];
+        rank += (o < me) || (o == me && j < i);
+    }
+    perm[rank] = (uint16_t)i;
+    __syncthreads();
+    v[i | ((int)perm[i] << 10)] = 0;
+}
+
 // ---------------------------------------------------------------------------
 // contiguous C0 tile: 3^g blocks x 8 words in shared memory
 
@@ -2105,6 +2125,32 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
     int rc;
     if ((rc = validate(n, 0))) return rc;
     return dqmc_gen3_range_device(values_dev, 0, 1ll << n, p_on, p_dc, seed, stream);
+}
+
+int dqmc_gen_sbox_device(uint8_t *values_dev, uint64_t seed, void *stream) {
+    int rc;
+    if (!values_dev) return set_err(DQMC_ERR_INVALID, "null output");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((rc = ensure_device())) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(values_dev, 1, (size_t)1 << 20, s));
+    k_sbox<<<1, 1024, 0, s>>>(values_dev, seed);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return DQMC_OK;
+}
+
+int dqmc_gen_sbox_host(uint8_t *values_host, uint64_t seed) {
+    int rc;
+    if (!values_host) return set_err(DQMC_ERR_INVALID, "null output");
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_device())) return rc;
+        if ((rc = grow(g_eng.in_tmp, g_eng.in_tmp_cap, (size_t)1 << 20, 1))) return rc;
+    }
+    if ((rc = dqmc_gen_sbox_device((uint8_t *)g_eng.in_tmp, seed, g_eng.stream))) return rc;
+    CK(cudaMemcpy(values_host, g_eng.in_tmp, (size_t)1 << 20, cudaMemcpyDeviceToHost));
+    return DQMC_OK;
 }
 
 int dqmc_gen3_host(uint8_t *values_host, int n, double p_on, double p_dc, uint64_t seed) {

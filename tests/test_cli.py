@@ -78,3 +78,43 @@ class TestGpu:
     def test_count_only_matches_readme(self, capsys):
         code, out, _ = run(["primes", "--n", "16", "--density", "0.5", "--seed", "42", "--count-only"], capsys)
         assert code == 0 and out.strip() == "68460"  # pkg/README.md:54-55
+
+    @pytest.mark.parametrize("cfg", [1, 2, 3])
+    def test_config_workloads(self, capsys, golden, cfg):
+        # BASELINE configs generated on the device (configs.py) -> golden prime counts
+        code, out, _ = run(["primes", "--config", str(cfg), "--count-only"], capsys)
+        assert code == 0 and int(out) == golden["configs"][str(cfg)]["primes"]
+
+
+@pytest.mark.gpu
+class TestDeviceGenerators:
+    """configs.py (product) against oracle/gen.py (checker), byte for byte."""
+
+    @pytest.mark.parametrize("cfg", [1, 2, 3])
+    def test_config_values(self, gen_mod, cfg):
+        from paper_2302_10083_b200 import configs
+
+        assert np.array_equal(configs.config_values_host(cfg), gen_mod.config_values(cfg))
+        assert np.array_equal(configs.config_values_device(cfg).cpu().numpy(), gen_mod.config_values(cfg))
+
+    def test_config4_distribution_small_n(self, gen_mod):
+        from paper_2302_10083_b200 import configs
+
+        assert np.array_equal(configs.config_values_host(4, n=14), gen_mod.config_values(4, n=14))
+
+    @pytest.mark.parametrize("seed", [0, 1, 7, 2**63 + 5])
+    def test_sbox_seeds(self, gen_mod, seed):
+        from paper_2302_10083_b200 import _lib
+
+        out = np.empty(1 << 20, dtype=np.uint8)
+        _lib.check(_lib.load().dqmc_gen_sbox_host(out.ctypes.data, seed))
+        ref = gen_mod.sbox_complement(seed)
+        assert np.array_equal(out, ref) and int((out == 0).sum()) == 1024
+
+    def test_bad_config(self):
+        from paper_2302_10083_b200 import configs
+
+        with pytest.raises(ValueError):
+            configs.config_values_host(3, n=18)
+        with pytest.raises(ValueError):
+            configs.config_values_host(9)
