@@ -174,6 +174,18 @@ int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int
                                int64_t ranks_cap, int64_t *count_out, uint32_t flags, void *stream);
 int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint64_t nbytes, int op, void *stream);
 
+/* Peer access for the sharded path's P2P transport (one process per GPU):
+ * a rank exports a CUDA IPC handle of the allocation holding one of its
+ * blocks, plus the block's byte offset inside it; a peer opens the handle
+ * (once per allocation) and passes base + offset straight to
+ * dqmc_bitop_device, so the AND / OR kernels read the peer's memory over
+ * NVLink with no staging copy. handle is 64 bytes
+ * (cudaIpcMemHandle_t). dqmc_ipc_open also enables peer access between the
+ * current device and the allocation's device when they differ. */
+int dqmc_ipc_get(const void *dev_ptr, void *handle_out, uint64_t *offset_out);
+int dqmc_ipc_open(const void *handle, void **base_out);
+int dqmc_ipc_close(void *base);
+
 /* The pass plan the engine runs for n variables (host logic, no GPU needed):
  * out = {ne, H, g, T, m, r[0..7], a[0..7], ib_C, ib_E, ib_D[0..7], rank_sub}
  * (32 int64 entries). Returns the number written. */

@@ -54,6 +54,9 @@ EXPORTS = (
     "dqmc_gen3_host",
     "dqmc_gen_sbox_device",
     "dqmc_gen_sbox_host",
+    "dqmc_ipc_get",
+    "dqmc_ipc_open",
+    "dqmc_ipc_close",
     "dqmc_order_by_weight",
     "dqmc_merge_device",
     "dqmc_reduce_extract_device",
@@ -142,6 +145,9 @@ def load() -> ctypes.CDLL:
             "dqmc_gen3_host": (i32, [vp, i32, dbl, dbl, u64]),
             "dqmc_gen_sbox_device": (i32, [vp, u64, vp]),
             "dqmc_gen_sbox_host": (i32, [vp, u64]),
+            "dqmc_ipc_get": (i32, [vp, vp, ctypes.POINTER(ctypes.c_uint64)]),
+            "dqmc_ipc_open": (i32, [vp, ctypes.POINTER(ctypes.c_void_p)]),
+            "dqmc_ipc_close": (i32, [vp]),
             "dqmc_order_by_weight": (i32, [vp, i64, i32, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
             "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),

@@ -1212,6 +1212,8 @@ struct PinnedBuf {
     size_t cap = 0;          // entries
 };
 
+typedef CUresult (*AddrRangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+
 struct Engine {
     int device = -1;
     cudaStream_t stream = nullptr;
@@ -1248,6 +1250,7 @@ struct Engine {
     bool attrs_set = false;
     int num_sms = 148;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    AddrRangeFn addr_range = nullptr;  // cuMemGetAddressRange (IPC offsets)
 };
 
 Engine g_eng;
@@ -2125,6 +2128,51 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
     int rc;
     if ((rc = validate(n, 0))) return rc;
     return dqmc_gen3_range_device(values_dev, 0, 1ll << n, p_on, p_dc, seed, stream);
+}
+
+int dqmc_ipc_get(const void *dev_ptr, void *handle_out, uint64_t *offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    int rc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_device())) return rc;
+        if (!g_eng.addr_range) {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) return set_err(DQMC_ERR_CUDA, "cuMemGetAddressRange unavailable");
+            g_eng.addr_range = (AddrRangeFn)fn;
+        }
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    const CUresult r = g_eng.addr_range(&base, &size, (CUdeviceptr)dev_ptr);
+    if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_INVALID, "not a device allocation: " + std::to_string((int)r));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void *)base));
+    memcpy(handle_out, &h, sizeof h);
+    *offset_out = (uint64_t)((CUdeviceptr)dev_ptr - base);
+    return DQMC_OK;
+}
+
+int dqmc_ipc_open(const void *handle, void **base_out) {
+    if (!handle || !base_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    int rc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_device())) return rc;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    CK(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return DQMC_OK;
+}
+
+int dqmc_ipc_close(void *base) {
+    if (!base) return set_err(DQMC_ERR_INVALID, "null pointer argument");
+    CK(cudaIpcCloseMemHandle(base));
+    return DQMC_OK;
 }
 
 int dqmc_gen_sbox_device(uint8_t *values_dev, uint64_t seed, void *stream) {

@@ -20,9 +20,17 @@ same map); each block computed at its owner, inputs exchanged point-to-point.
 NCCL has no bitwise-AND reduction (nccl.h ops: sum/prod/max/min/avg), so the
 exchange is send/recv of whole blocks and the AND/OR runs in our kernels.
 
-The same schedule runs over a real process group (``DistComm``: torch.distributed,
-NCCL on GPUs, gloo on CPU for the tests) or over all 2^k ranks inside one
-process (``EmulatedComm``), which lets one GPU check k-GPU bit-exactness.
+The same schedule runs over a real process group, or over all 2^k ranks inside
+one process (``EmulatedComm``), which lets one GPU check k-GPU bit-exactness.
+Transports for a process group:
+  ``DistComm``  torch.distributed send/recv of whole blocks (NCCL on GPUs;
+                gloo with host staging for CPU tests and GPU-sharing tests);
+  ``IpcComm``   P2P: no transfer at all. Each rank exports CUDA IPC handles of
+                the blocks peers need; the peer opens them and our AND / OR
+                kernels read the owner's memory directly over NVLink (the
+                survey's fused peer-load design). Host-side
+                all_gather / barrier order the rounds; no kernel ever waits
+                on another process.
 Local compute is an ``ops`` object: ``GpuOps`` (libdqmc.so) in production;
 tests may pass a CPU implementation to exercise the host logic under gloo.
 """
@@ -132,6 +140,9 @@ class EmulatedComm:
     def exchange(self, transfers, held, ops):
         return {(dst, c): held[(src, c)] for c, src, dst in transfers}
 
+    def done_reading(self, ops):
+        pass
+
     def barrier(self):
         pass
 
@@ -188,8 +199,76 @@ class DistComm:
         ops.sync()
         return out
 
+    def done_reading(self, ops):
+        pass  # received blocks are private copies
+
     def barrier(self):
         self.dist.barrier(group=self.group)
+
+
+class PeerBlock:
+    """A block that lives in a peer process's device memory (opened via CUDA
+    IPC): duck-types the two tensor methods the block ops use."""
+
+    def __init__(self, ptr: int, numel: int):
+        self._ptr, self._numel = ptr, numel
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+    def numel(self) -> int:
+        return self._numel
+
+
+class IpcComm(DistComm):
+    """P2P transport over CUDA IPC (see the module docstring). Round protocol:
+    every rank finishes its stream, then all-gathers (block, owner, handle,
+    offset) for the blocks others need; consumers open each peer allocation
+    once and read it in place. ``done_reading`` (sync + barrier) fences the
+    owners' in-place REDUCE behind the peers' last reads."""
+
+    def __init__(self, group=None):
+        super().__init__(group, staging=False)
+        from . import _lib
+
+        self._lib = _lib
+        self._opened: dict = {}  # (owner rank, owner base address) -> local base pointer
+
+    def exchange(self, transfers, held, ops):
+        import ctypes
+
+        L = self._lib.load()
+        ops.sync()  # blocks peers will read are complete before anyone reads them
+        mine = []
+        for c, src, dst in transfers:
+            if src == self.rank:
+                t = held[(src, c)]
+                h = ctypes.create_string_buffer(64)
+                off = ctypes.c_uint64(0)
+                self._lib.check(L.dqmc_ipc_get(t.data_ptr(), h, ctypes.byref(off)))
+                mine.append((c, dst, h.raw, int(off.value), t.data_ptr() - int(off.value), int(t.numel())))
+        allx = [None] * self.world
+        self.dist.all_gather_object(allx, mine, group=self.group)
+        out = {}
+        for src, lst in enumerate(allx):
+            for c, dst, hb, off, base_id, numel in lst:
+                if dst != self.rank:
+                    continue
+                key = (src, base_id)
+                if key not in self._opened:
+                    p = ctypes.c_void_p()
+                    self._lib.check(L.dqmc_ipc_open(hb, ctypes.byref(p)))
+                    self._opened[key] = int(p.value)
+                out[(dst, c)] = PeerBlock(self._opened[key] + off, numel)
+        return out
+
+    def done_reading(self, ops):
+        ops.sync()
+        self.dist.barrier(group=self.group)
+        L = self._lib.load()
+        for base in self._opened.values():
+            self._lib.check(L.dqmc_ipc_close(base))
+        self._opened.clear()
 
 
 def _dedupe(transfers: Iterable[tuple]) -> list[tuple]:
@@ -244,6 +323,7 @@ def sharded_prime_ranks(inputs: dict, n: int, k: int, ops, comm) -> dict:
         kills[t] = kill
     del recv
     ops.sync()
+    comm.done_reading(ops)  # P2P: peers have read every M_t before it is reduced in place
     # (4) reduce the low dimensions, apply the kills, compact with the block offset
     out = {}
     for t in all_blocks(k):
@@ -308,7 +388,9 @@ class GpuOps:
         return self._bitop(dst, src, 1, out=dst)
 
     def copy(self, src):
-        return src.clone()
+        if isinstance(src, self.torch.Tensor):
+            return src.clone()
+        return self._bitop(src, src, 0)  # a peer block: x & x, read over P2P
 
     def reduce_extract(self, block, nl, kill, offset):
         import ctypes
@@ -373,7 +455,11 @@ def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
                                                    workload["p_dc"], workload["seed"],
                                                    torch.cuda.current_stream().cuda_stream))
     ops = GpuOps(nl)
-    comm = DistComm(staging=backend != "nccl")
+    # DQMC_DIST_TRANSPORT=p2p: CUDA-IPC peer reads (IpcComm); default: block send/recv
+    if os.environ.get("DQMC_DIST_TRANSPORT", "sendrecv") == "p2p":
+        comm = IpcComm()
+    else:
+        comm = DistComm(staging=backend != "nccl")
 
     def step():
         parts = sharded_prime_ranks({rank: vals}, n, k, ops, comm)

@@ -176,9 +176,10 @@ def test_gpu_emulated_config4_k3(pkg, golden):
     assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()[:16] == g["ranks_sha256_prefix"]
 
 
-def _gpu_worker(rank, world, port, n, outdir):
-    """One rank of a 2-process run sharing cuda:0: real GPU block ops, host-staged
-    gloo exchange (no kernel waits on the other process)."""
+def _gpu_worker(rank, world, port, n, outdir, transport="staging"):
+    """One rank of a multi-process run sharing cuda:0: real GPU block ops; the
+    exchange is host-staged gloo send/recv, or P2P reads of the peers' blocks
+    through CUDA IPC (no kernel waits on another process either way)."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -191,7 +192,8 @@ def _gpu_worker(rank, world, port, n, outdir):
         vals = torch.empty(1 << nl, dtype=torch.uint8, device="cuda")
         _lib.check(_lib.load().dqmc_gen3_range_device(vals.data_ptr(), rank << nl, 1 << nl, 0.75, 0.05, 3,
                                                        torch.cuda.current_stream().cuda_stream))
-        parts = S.sharded_prime_ranks({rank: vals}, n, k, S.GpuOps(nl), S.DistComm(staging=True))
+        comm = S.IpcComm() if transport == "p2p" else S.DistComm(staging=True)
+        parts = S.sharded_prime_ranks({rank: vals}, n, k, S.GpuOps(nl), comm)
         gathered = [None] * world if rank == 0 else None
         dist.gather_object({t: v.cpu().numpy() for t, v in parts.items()}, gathered, dst=0)
         if rank == 0:
@@ -204,27 +206,31 @@ def _gpu_worker(rank, world, port, n, outdir):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["staging", "p2p"])
 @pytest.mark.parametrize("world,n", [(2, 18), (4, 19)])
-def test_gpu_multiprocess_sharded(world, n, tmp_path, pkg):
-    """The DistComm data path with GpuOps on real kernels, ranks as processes."""
+def test_gpu_multiprocess_sharded(world, n, transport, tmp_path, pkg):
+    """The sharded data path with GpuOps on real kernels, ranks as processes,
+    over both transports (send/recv with host staging; CUDA-IPC peer reads)."""
     from paper_2302_10083_b200 import device
 
-    mp.spawn(_gpu_worker, args=(world, _free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_gpu_worker, args=(world, _free_port(), n, str(tmp_path), transport), nprocs=world, join=True)
     got = np.load(tmp_path / "ranks.npy")
     want = pkg.prime_ranks_from_values(device.gen3_device(n, 0.75, 0.05, 3).cpu().numpy())
     assert np.array_equal(got, want), _block_diff(got, want, n, world.bit_length() - 1)
 
 
 @pytest.mark.gpu
-def test_bench_torchrun_two_ranks_gloo(tmp_path, pkg):
+@pytest.mark.parametrize("transport", ["sendrecv", "p2p"])
+def test_bench_torchrun_two_ranks_gloo(transport, tmp_path, pkg):
     """bench.py under torch.distributed.run (N=2) through the sharded path, gloo
-    backend with host staging so both ranks can share this run's single GPU."""
+    backend (host-staged send/recv, or CUDA-IPC peer reads) so both ranks can
+    share this run's single GPU."""
     import json
     import subprocess
     import sys
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DQMC_DIST_BACKEND="gloo")
+    env = dict(os.environ, DQMC_DIST_BACKEND="gloo", DQMC_DIST_TRANSPORT=transport)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1", "--nvars", "18"]
