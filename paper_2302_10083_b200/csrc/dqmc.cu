@@ -372,13 +372,26 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
         int64_t pos = run + (incl - cnt);
         run += __shfl_sync(0xffffffffu, incl, 31);
         const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+        int64_t *o = fa.out + pos;
+        if (pos + cnt <= fa.cap) {
+            // the block as four 64-bit words: half the loops of a 32-bit walk
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            uint32_t w = wv[k];
-            while (w) {
-                if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
-                pos++;
-                w &= w - 1;
+            for (int k = 0; k < 4; k++) {
+                uint64_t w = ((uint64_t)wv[2 * k + 1] << 32) | wv[2 * k];
+                while (w) {
+                    *o++ = rbase + k * 64 + (__ffsll((long long)w) - 1);
+                    w &= w - 1;
+                }
+            }
+        } else {  // the scratch is too small: write what fits (the host grows it and reruns)
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                uint32_t w = wv[k];
+                while (w) {
+                    if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                    pos++;
+                    w &= w - 1;
+                }
             }
         }
     }
