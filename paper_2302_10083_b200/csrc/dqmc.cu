@@ -463,7 +463,19 @@ __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scr
         // a tile whose range overflowed the scratch is skipped: the host sees
         // total > scratch capacity, grows the scratch and reruns the final stage
         if (c < 0 || src < 0 || src + c > scap) continue;
-        for (int i = lane; i < c; i += 32)
+        int i = lane;
+        if (dst + c <= cap) {
+            // four independent loads in flight per lane (the copy is latency-bound)
+            for (; i + 96 < c; i += 128) {
+                const int64_t a0 = __ldcs(scratch + src + i), a1 = __ldcs(scratch + src + i + 32);
+                const int64_t a2 = __ldcs(scratch + src + i + 64), a3 = __ldcs(scratch + src + i + 96);
+                out[dst + i] = a0;
+                out[dst + i + 32] = a1;
+                out[dst + i + 64] = a2;
+                out[dst + i + 96] = a3;
+            }
+        }
+        for (; i < c; i += 32)
             if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
     }
 }
