@@ -6,6 +6,17 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// wide variant: an item covers W adjacent 128-B columns of every row
+__global__ void k_write_wide(uint4 *s, int64_t Qv, int64_t ncolw, int64_t nitems, int rows, int W) {
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int64_t col = it % ncolw, outer = it / ncolw;
+        uint4 *base = s + outer * rows * Qv + col * 8 * W;
+        const int per = 8 * W;
+        for (int i = t; i < rows * per; i += nt) base[(i / per) * Qv + (i % per)] = make_uint4(it, i, 0, 0);
+    }
+}
+
 __global__ void k_write(uint4 *s, int64_t Qv, int64_t ncol, int64_t nitems, int rows, int contiguous) {
     const int t = threadIdx.x, nt = blockDim.x;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -29,6 +40,24 @@ int main() {
     const int64_t total_blocks = far_blocks * rows;
     uint4 *s;
     if (cudaMalloc(&s, total_blocks * 32)) { printf("alloc failed\n"); return 1; }
+    for (int W = 1; W <= 16; W *= 2) {  // far stride, W columns per item
+        const int64_t Qb = far_blocks, Qv = Qb * 2, ncolw = Qb / (4 * W), nitems = ncolw * (total_blocks / (Qb * rows));
+        float best = 1e9;
+        for (int rep = 0; rep < 3; rep++) {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            k_write_wide<<<148, 1024>>>(s, Qv, ncolw, nitems, rows, W);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double bytes = (double)nitems * rows * 128 * W;
+        printf("far stride, %2d columns (%4d B) per row per item: %.2f ms, %.0f GB/s\n", W, 128 * W, best, bytes / (best / 1e3) / 1e9);
+    }
     for (int grid_mul = 1; grid_mul <= 4; grid_mul *= 2)
     for (int v = 0; v < 3; v++) {
         const int64_t Qb = v == 0 ? far_blocks : near_blocks;
