@@ -91,6 +91,19 @@ int dqmc_primes_u8(const uint8_t *values, int n, int h, uint64_t mem_cap, uint32
                    dqmc_result_t *out);
 void dqmc_free_result(dqmc_result_t *res);
 
+/* The same calls as a stream of jobs (at most two outstanding, collected in
+ * submission order). dqmc_submit_* queues the table's H2D, every pass and the
+ * final stage, and returns; dqmc_collect waits for that job and copies its
+ * ranks to the host while the device already runs the next job, so call i's
+ * D2H overlaps call i+1's passes. The input must stay valid and unchanged
+ * until the job is collected. The first job of an n runs synchronously inside
+ * submit (its count sizes the outputs of the next ones); the result is the
+ * same as dqmc_primes_tt / dqmc_primes_u8 with h = 0, no cap. flags: as for
+ * those (COUNT_ONLY / KEEP_BITMAP / TIMING jobs run synchronously). */
+int dqmc_submit_tt(const uint64_t *tt_words, int n, uint32_t flags, int64_t *job);
+int dqmc_submit_u8(const uint8_t *values, int n, uint32_t flags, int64_t *job);
+int dqmc_collect(int64_t job, dqmc_result_t *out);
+
 /* Same computation with DEVICE-resident input and output (bench `value`,
  * torch integration). ranks_dev may be NULL (count only). If the count
  * exceeds ranks_cap, *count_out is the true count and nothing beyond

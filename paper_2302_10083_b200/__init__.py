@@ -10,6 +10,7 @@ from .dense import (
     DEFAULT_SPLIT,
     MERGE,
     REDUCE,
+    PrimeJob,
     block_bits_for,
     count_primes,
     dense_prime_ranks,
@@ -17,6 +18,8 @@ from .dense import (
     prime_bitmap,
     prime_ranks_from_values,
     state_bytes,
+    stream_prime_ranks,
+    submit,
 )
 from .engine import ENGINES, run_engine
 from .errors import ImplicantsError, ParseError, ResourceLimitError
@@ -42,6 +45,7 @@ __all__ = [
     "MAX_N",
     "MERGE",
     "ParseError",
+    "PrimeJob",
     "REDUCE",
     "ResourceLimitError",
     "SYMBOLS",
@@ -58,6 +62,8 @@ __all__ = [
     "rank_weights",
     "ranks_to_text",
     "run_engine",
+    "stream_prime_ranks",
+    "submit",
     "state_bytes",
     "unrank",
     "unrank_many",

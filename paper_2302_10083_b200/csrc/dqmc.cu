@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1239,6 +1240,16 @@ struct PinnedBuf {
 
 typedef CUresult (*AddrRangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
 
+// a submitted host-API job (dqmc_submit_* / dqmc_collect)
+struct Job {
+    int64_t id = 0;
+    int slot = -1;        // -1: ran synchronously at submit, result in `res`
+    dqmc_result_t res{};  // sync jobs only
+    const void *in = nullptr;
+    int kind = 0, n = 0;
+    uint32_t flags = 0;
+};
+
 struct Engine {
     int device = -1;
     cudaStream_t stream = nullptr;
@@ -1276,6 +1287,15 @@ struct Engine {
     int num_sms = 148;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     AddrRangeFn addr_range = nullptr;  // cuMemGetAddressRange (IPC offsets)
+    // submit/collect: at most two jobs in flight, one slot each
+    std::deque<Job> jobs;
+    int64_t next_job = 0;
+    void *jin[2] = {nullptr, nullptr};
+    size_t jin_cap[2] = {0, 0};  // bytes
+    int64_t *jranks[2] = {nullptr, nullptr};
+    size_t jranks_cap[2] = {0, 0};  // entries
+    int64_t *jcount_host = nullptr;  // pinned, one count per slot
+    cudaEvent_t jev[2] = {nullptr, nullptr};
 };
 
 Engine g_eng;
@@ -2016,6 +2036,111 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
     return DQMC_OK;
 }
 
+// Host-API jobs, two in flight: submit queues the H2D of the table, every pass
+// and the final stage on the engine stream and returns; collect waits for the
+// job's final stage, then copies its ranks to pinned host memory on the copy
+// stream while the engine stream already runs the next job. A stream of calls
+// thus overlaps call i's D2H with call i+1's passes. The first job of an n (no
+// count hint yet to size the outputs) runs synchronously inside submit.
+int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *job_out) {
+    if (!job_out) return set_err(DQMC_ERR_INVALID, "null job pointer");
+    int rc;
+    if ((rc = validate(n, 0))) return rc;
+    if (!host_in) return set_err(DQMC_ERR_INVALID, "null input pointer");
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_device())) return rc;
+        if ((rc = ensure_attrs())) return rc;
+        if (g_eng.jobs.size() >= 2) return set_err(DQMC_ERR_INVALID, "two jobs outstanding: collect the oldest first");
+        const Plan p = make_plan(n);
+        const bool async = !(flags & (DQMC_FLAG_COUNT_ONLY | DQMC_FLAG_KEEP_BITMAP | DQMC_FLAG_TIMING)) && p.T > 0 &&
+                           g_eng.hint_n == n && g_eng.hint_count > 0;
+        if (async) {
+            if ((rc = check_cap(n, 0, 0, engine_device_bytes(p, false)))) return rc;
+            const int64_t id = g_eng.next_job++;
+            const int slot = (int)(id & 1);
+            if (!g_eng.jcount_host) CK(cudaHostAlloc((void **)&g_eng.jcount_host, 2 * sizeof(int64_t), cudaHostAllocDefault));
+            if (!g_eng.jev[slot]) CK(cudaEventCreateWithFlags(&g_eng.jev[slot], cudaEventDisableTiming));
+            const size_t in_bytes =
+                kind == DQMC_IN_U8 ? ((size_t)1 << n) : (size_t)std::max<int64_t>(1, (1ll << n) / 64) * 8;
+            if ((rc = grow(g_eng.jin[slot], g_eng.jin_cap[slot], std::max<size_t>(in_bytes, 8), 1))) return rc;
+            const size_t want = (size_t)((double)g_eng.hint_count * 1.05) + 4096;
+            if ((rc = grow(g_eng.jranks[slot], g_eng.jranks_cap[slot], want, 8))) return rc;
+            g_eng.scratch_want = std::max(g_eng.scratch_want, want);
+            if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.nblocks * 32, 1))) return rc;
+            cudaStream_t s = g_eng.stream;
+            CK(cudaMemcpyAsync(g_eng.jin[slot], host_in, in_bytes, cudaMemcpyHostToDevice, s));
+            const uint32_t *tt32 = nullptr;
+            if ((rc = input_words(g_eng.jin[slot], kind, n, &tt32, s))) return rc;
+            Timer tm{false, s};
+            if ((rc = run_merge(p, tt32, g_eng.state, false, tm, s))) return rc;
+            if ((rc = run_reduce(p, g_eng.state, true, tm, s))) return rc;
+            int64_t unused = 0;
+            int64_t *cdev = g_eng.total + 8 + slot;  // device count of this slot (-(count+1): outputs too small)
+            if ((rc = run_final(p, nullptr, g_eng.state, nullptr, p.ib_E, -p.rank_sub, g_eng.jranks[slot],
+                                (int64_t)g_eng.jranks_cap[slot], false, nullptr, &unused, tm, s, cdev)))
+                return rc;
+            CK(cudaMemcpyAsync(g_eng.jcount_host + slot, cdev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            CK(cudaEventRecord(g_eng.jev[slot], s));
+            Job j;
+            j.id = id;
+            j.slot = slot;
+            j.in = host_in;
+            j.kind = kind;
+            j.n = n;
+            j.flags = flags;
+            g_eng.jobs.push_back(j);
+            *job_out = id;
+            return DQMC_OK;
+        }
+    }
+    dqmc_result_t res{};
+    if ((rc = primes_host_impl(host_in, kind, n, 0, 0, flags, &res))) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Job j;
+    j.id = g_eng.next_job++;
+    j.res = res;
+    g_eng.jobs.push_back(j);
+    *job_out = j.id;
+    return DQMC_OK;
+}
+
+int collect_impl(int64_t job, dqmc_result_t *out) {
+    if (!out) return set_err(DQMC_ERR_INVALID, "null result pointer");
+    out->count = 0;
+    out->ranks = nullptr;
+    out->_owner = nullptr;
+    std::unique_lock<std::mutex> lk(g_mu);
+    if (g_eng.jobs.empty() || g_eng.jobs.front().id != job)
+        return set_err(DQMC_ERR_INVALID, "unknown job, or jobs collected out of submission order");
+    const Job j = g_eng.jobs.front();
+    g_eng.jobs.pop_front();
+    if (j.slot < 0) {
+        *out = j.res;
+        return DQMC_OK;
+    }
+    CK(cudaEventSynchronize(g_eng.jev[j.slot]));
+    const int64_t c = g_eng.jcount_host[j.slot];
+    if (c < 0) {  // the hinted output was too small: run this job again, synchronously
+        g_eng.hint_count = -c - 1;
+        g_eng.scratch_want = std::max(g_eng.scratch_want, (size_t)((double)(-c - 1) * 1.05) + 4096);
+        lk.unlock();
+        return primes_host_impl(j.in, j.kind, j.n, 0, 0, j.flags, out);
+    }
+    g_eng.hint_count = c;
+    if (c > 0) {
+        PinnedBuf pb;
+        int rc;
+        if ((rc = alloc_pinned((size_t)c, pb))) return rc;
+        CK(cudaMemcpyAsync(pb.ptr, g_eng.jranks[j.slot], (size_t)c * 8, cudaMemcpyDeviceToHost, g_eng.stream2));
+        CK(cudaStreamSynchronize(g_eng.stream2));
+        out->count = c;
+        out->ranks = pb.ptr;
+        out->_owner = new PinnedBuf(pb);
+    }
+    return DQMC_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -2154,6 +2279,16 @@ int dqmc_gen3_device(uint8_t *values_dev, int n, double p_on, double p_dc, uint6
     if ((rc = validate(n, 0))) return rc;
     return dqmc_gen3_range_device(values_dev, 0, 1ll << n, p_on, p_dc, seed, stream);
 }
+
+int dqmc_submit_tt(const uint64_t *tt_words, int n, uint32_t flags, int64_t *job) {
+    return submit_impl(tt_words, DQMC_IN_WORDS, n, flags, job);
+}
+
+int dqmc_submit_u8(const uint8_t *values, int n, uint32_t flags, int64_t *job) {
+    return submit_impl(values, DQMC_IN_U8, n, flags, job);
+}
+
+int dqmc_collect(int64_t job, dqmc_result_t *out) { return collect_impl(job, out); }
 
 int dqmc_ipc_get(const void *dev_ptr, void *handle_out, uint64_t *offset_out) {
     if (!dev_ptr || !handle_out || !offset_out) return set_err(DQMC_ERR_INVALID, "null pointer argument");
@@ -2369,6 +2504,12 @@ void dqmc_release(void) {
         if (g_eng.chunk_ev[i]) cudaEventDestroy(g_eng.chunk_ev[i]);
     cudaFree(g_eng.chunk_base);
     if (g_eng.hbase) cudaFreeHost(g_eng.hbase);
+    for (int i = 0; i < 2; i++) {
+        cudaFree(g_eng.jin[i]);
+        cudaFree(g_eng.jranks[i]);
+        if (g_eng.jev[i]) cudaEventDestroy(g_eng.jev[i]);
+    }
+    if (g_eng.jcount_host) cudaFreeHost(g_eng.jcount_host);
     g_eng = Engine();
 }
 

@@ -115,6 +115,54 @@ def prime_ranks_from_values(
     return _lib.result_to_array(res)
 
 
+class PrimeJob:
+    """A submitted call (dqmc_submit_*): ``result()`` waits for it and returns
+    the int64 ranks. Keeps its input alive until collected. At most two jobs
+    may be outstanding; they are collected in submission order."""
+
+    def __init__(self, job_id: int, keep):
+        self.id = job_id
+        self._keep = keep
+        self._done = None
+
+    def result(self) -> np.ndarray:
+        if self._done is None:
+            res = _lib.DqmcResult()
+            _lib.check(_lib.load().dqmc_collect(self.id, ctypes.byref(res)))
+            self._done = _lib.result_to_array(res)
+            self._keep = None
+        return self._done
+
+
+def submit(table) -> PrimeJob:
+    """Queue one call: a TruthTable (or anything with .n/.words), or a uint8
+    three-valued table (0 off / 1 on / 2 don't-care, 2^n entries)."""
+    L = _lib.load()
+    job = ctypes.c_int64(0)
+    if isinstance(table, np.ndarray) and table.dtype == np.uint8:
+        v = np.ascontiguousarray(table)
+        n = int(len(v)).bit_length() - 1
+        if len(v) != (1 << n) or not 1 <= n <= 31:
+            raise ValueError(f"expected 2^n values, got {len(v)}")
+        _lib.check(L.dqmc_submit_u8(v.ctypes.data, n, 0, ctypes.byref(job)))
+        return PrimeJob(job.value, v)
+    n, words = _as_words(table)
+    _lib.check(L.dqmc_submit_tt(words.ctypes.data, n, 0, ctypes.byref(job)))
+    return PrimeJob(job.value, words)
+
+
+def stream_prime_ranks(tables):
+    """Prime ranks of every table of an iterable, in order, with two calls in
+    flight: call i's device-to-host copy overlaps call i+1's passes."""
+    pending = []
+    for t in tables:
+        pending.append(submit(t))
+        if len(pending) == 2:
+            yield pending.pop(0).result()
+    while pending:
+        yield pending.pop(0).result()
+
+
 def find_primes_dense(
     tt: TruthTable,
     h: int | None = None,

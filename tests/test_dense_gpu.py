@@ -289,3 +289,42 @@ class TestAsyncAndGraph:
         else:
             with pytest.raises(RuntimeError):
                 g.ranks()
+
+
+class TestJobStream:
+    """dqmc_submit_* / dqmc_collect: two calls in flight, results identical to
+    the synchronous call, edge cases of the job protocol."""
+
+    def test_stream_matches_sync(self, pkg, gen_mod):
+        tabs = [gen_mod.gen3(n, 0.7, 0.05, s) for n, s in ((16, 1), (16, 2), (16, 3), (18, 4), (18, 5), (16, 6))]
+        want = [pkg.prime_ranks_from_values(t) for t in tabs]
+        got = list(pkg.stream_prime_ranks(tabs))
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+    def test_truth_tables_and_repeat(self, pkg, gen_mod):
+        t = pkg.TruthTable(17, gen_mod.random_words(17, 0.6, 9))
+        want = pkg.dense_prime_ranks(t)
+        for r in pkg.stream_prime_ranks([t] * 5):
+            assert np.array_equal(r, want)
+
+    def test_output_outgrows_the_hint(self, pkg, gen_mod):
+        # a sparse table first (small hint), then a dense one of the same n:
+        # the second job overflows its hinted output and is recomputed
+        small = gen_mod.gen3(18, 0.05, 0.0, 1)
+        big = gen_mod.gen3(18, 0.8, 0.1, 2)
+        want = [pkg.prime_ranks_from_values(x) for x in (small, big, big)]
+        got = list(pkg.stream_prime_ranks([small, small, big, big]))
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[0])
+        assert np.array_equal(got[2], want[1]) and np.array_equal(got[3], want[2])
+
+    def test_protocol_errors(self, pkg, gen_mod):
+        t = gen_mod.gen3(12, 0.5, 0.0, 1)
+        a, b = pkg.submit(t), pkg.submit(t)
+        with pytest.raises(ValueError):
+            pkg.submit(t)  # a third outstanding job
+        with pytest.raises(ValueError):
+            b.result()  # out of order
+        ra, rb = a.result(), b.result()
+        assert np.array_equal(ra, rb) and np.array_equal(ra, pkg.prime_ranks_from_values(t))
