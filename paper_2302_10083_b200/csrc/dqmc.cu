@@ -848,16 +848,29 @@ __device__ __forceinline__ void bar_compute(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// Columns per tile: a group of 3^r rows with r < 6 packs CC adjacent 128-B
+// columns into one tile, so tiles stay ~90 KB (enough bytes in flight per SM)
+// and rows are written CC x 128 B wide (far-stride rows stream at ~4.1 TB/s in
+// 128-B pieces, ~5.9 TB/s in 256-B and wider pieces; tools/probes/). The TMA
+// box limit (256 elements) caps CC at 8.
 template <int R1, int R2>
+__host__ __device__ constexpr int pipe_cols() {
+    constexpr int nr = P3<R1>::v * P3<R2>::v;
+    return nr >= 729 ? 1 : (729 / nr > 8 ? 8 : 729 / nr);
+}
+
+template <int R1, int R2, int CC = pipe_cols<R1, R2>()>
 struct PipeSmem {
     static constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v;
     static constexpr int NR = N1 * N2;
-    static constexpr int TILE_WORDS = NR * 32;
-    static constexpr int STAGE_WORDS = (1 << R1) * (1 << R2) * 32;
+    static constexpr int PITCH = 32 * CC;  // words per tile row
+    static constexpr int TILE_WORDS = NR * PITCH;
+    static constexpr int STAGE_WORDS = (1 << R1) * (1 << R2) * PITCH;
     static constexpr int BOXR = NR > 243 ? 243 : NR;  // TMA box rows (<= 256)
     static constexpr int NBOX = NR / BOXR;
-    // one register sub-cube task per compute warp per round
-    static constexpr int CW = (N1 > N2 ? N1 : N2) < 4 ? 4 : (N1 > N2 ? N1 : N2);
+    // compute warps: one register sub-cube task per warp per round (up to 27)
+    static constexpr int TASKS = (N1 > N2 ? N1 : N2) * CC;
+    static constexpr int CW = TASKS < 4 ? 4 : (TASKS > 27 ? 27 : TASKS);
     static constexpr int THREADS = (CW + 1) * 32;
     static constexpr int SMEM = (2 * TILE_WORDS + 2 * STAGE_WORDS) * 4;
 };
@@ -879,6 +892,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
     constexpr int CW = SM::CW;
+    constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t full[2], computed[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -905,16 +919,16 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 if (st) {
                     const int64_t it = item(i - 2);
                     mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
-                    const int c0 = (int)((it % ncol) * 32), c2 = (int)(it / ncol);
+                    const int c0 = (int)((it % ncol) * 32 * CC), c2 = (int)(it / ncol);
 #pragma unroll
                     for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
-                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile + x * SM::BOXR * 32);
+                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile + x * SM::BOXR * PITCH);
                         bulk_commit();
                     }
                 }
                 if (i < L) {
                     const int64_t it = item(i);
-                    const int c0 = (int)((it % ncol) * 32), outer = (int)(it / ncol);
+                    const int c0 = (int)((it % ncol) * 32 * CC), outer = (int)(it / ncol);
                     if (MODE == REDUCE_ONLY) {
                         // each box is reloaded as soon as its store has read it out of
                         // smem: the next tile's load overlaps the previous tile's store
@@ -927,7 +941,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                                 else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
                                 else bulk_wait_read<0>();
                             }
-                            tma_load_3d(tile + x * SM::BOXR * 32, &tmap, c0, x * SM::BOXR, outer, &full[b]);
+                            tma_load_3d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, outer, &full[b]);
                         }
                     } else {
                         // binary rows: one 5-D box {32 words, 2, .., 2} per binary rho2; the
@@ -938,7 +952,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                         mbar_expect_tx(&full[b], SM::STAGE_WORDS * 4);
 #pragma unroll
                         for (int b2 = 0; b2 < B2; b2++)
-                            tma_load_5d(stg + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
+                            tma_load_5d(stg + b2 * B1 * PITCH, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
                     }
                 }
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
@@ -957,62 +971,67 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
         if (MODE == MERGE_REDUCE) {
             const int sb = 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
             // round 1: merge the R1 axes for each binary rho2
-            for (int t2 = warp; t2 < B2; t2 += CW) {
+            for (int tt = warp; tt < B2 * CC; tt += CW) {
+                const int t2 = tt % B2, h = tt / B2;
                 const int r2 = bin_to_tern(t2);
                 uint32_t v[N1];
 #pragma unroll
                 for (int x = 0; x < N1; x++) v[x] = 0;
 #pragma unroll
-                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * 32 + lane];
+                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * PITCH + 32 * h + lane];
                 cube_merge<R1>(v);
                 if (R2 == 0) cube_reduce_par<R1>(v);
 #pragma unroll
-                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * 32 + lane] = v[x];
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * PITCH + 32 * h + lane] = v[x];
             }
             if (R2 > 0) {
                 bar_compute(NCT);
                 // round 2: merge + reduce the R2 axes
-                for (int t1 = warp; t1 < N1; t1 += CW) {
+                for (int tt = warp; tt < N1 * CC; tt += CW) {
+                const int t1 = tt % N1, h = tt / N1;
                     uint32_t v[N2];
 #pragma unroll
                     for (int x = 0; x < N2; x++) v[x] = 0;
 #pragma unroll
-                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * 32 + lane];
+                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * PITCH + 32 * h + lane];
                     cube_merge<R2>(v);
                     cube_reduce_par<R2>(v);
 #pragma unroll
-                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
+                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
                 }
                 bar_compute(NCT);
                 // round 3: reduce the R1 axes
-                for (int t2 = warp; t2 < N2; t2 += CW) {
+                for (int tt = warp; tt < N2 * CC; tt += CW) {
+                const int t2 = tt % N2, h = tt / N2;
                     uint32_t v[N1];
 #pragma unroll
-                    for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
+                    for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
                     cube_reduce_par<R1>(v);
 #pragma unroll
-                    for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
+                    for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
                 }
             }
         } else {
             // round 1: reduce the R1 axes
-            for (int t2 = warp; t2 < N2; t2 += CW) {
+            for (int tt = warp; tt < N2 * CC; tt += CW) {
+                const int t2 = tt % N2, h = tt / N2;
                 uint32_t v[N1];
 #pragma unroll
-                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
+                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
                 cube_reduce_par<R1>(v);
 #pragma unroll
-                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
             }
             if (R2 > 0) {
                 bar_compute(NCT);
-                for (int t1 = warp; t1 < N1; t1 += CW) {
+                for (int tt = warp; tt < N1 * CC; tt += CW) {
+                const int t1 = tt % N1, h = tt / N1;
                     uint32_t v[N2];
 #pragma unroll
-                    for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * 32 + lane];
+                    for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane];
                     cube_reduce_par<R2>(v);
 #pragma unroll
-                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
+                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
                 }
             }
         }
@@ -1023,7 +1042,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+            for (int t = threadIdx.x; t < NR * kRowBlocks * CC; t += NCT) {
                 uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
                 const uint4 x0 = p[0], x1 = p[1];
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
@@ -1050,6 +1069,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
     constexpr int CW = SM::CW;
+    constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t stage_full[2], stage_free[2], tile_done[2], tile_free[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1071,12 +1091,12 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
                 const int b = (int)(i & 1);
                 if (i >= 2) mbar_wait(&stage_free[b], (unsigned)(((i - 2) >> 1) & 1));
                 const int64_t it = blockIdx.x + i * gridDim.x;
-                const int c0 = (int)((it % ncol) * 32);
+                const int c0 = (int)((it % ncol) * 32 * CC);
                 uint32_t *st = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
                 mbar_expect_tx(&stage_full[b], SM::STAGE_WORDS * 4);
 #pragma unroll
                 for (int b2 = 0; b2 < B2; b2++)
-                    tma_load_5d(st + b2 * B1 * 32, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &stage_full[b]);
+                    tma_load_5d(st + b2 * B1 * PITCH, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &stage_full[b]);
             }
         }
         return;
@@ -1088,9 +1108,9 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
                 const int64_t it = blockIdx.x + i * gridDim.x;
                 mbar_wait(&tile_done[b], (unsigned)((i >> 1) & 1));
                 const uint32_t *tile = smem + b * SM::TILE_WORDS;
-                const int c0 = (int)((it % ncol) * 32);
+                const int c0 = (int)((it % ncol) * 32 * CC);
 #pragma unroll
-                for (int x = 0; x < SM::NBOX; x++) tma_store_3d(&tmap, c0, x * SM::BOXR, 0, tile + x * SM::BOXR * 32);
+                for (int x = 0; x < SM::NBOX; x++) tma_store_3d(&tmap, c0, x * SM::BOXR, 0, tile + x * SM::BOXR * PITCH);
                 bulk_commit();
                 bulk_wait_read0();
                 mbar_arrive(&tile_free[b]);
@@ -1109,41 +1129,44 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
         mbar_wait(&stage_full[b], (unsigned)((i >> 1) & 1));
         if (i >= 2) mbar_wait(&tile_free[b], (unsigned)(((i - 2) >> 1) & 1));
         // round 1: merge the R1 axes for each binary rho2 (stage -> tile)
-        for (int t2 = warp; t2 < B2; t2 += CW) {
+        for (int tt = warp; tt < B2 * CC; tt += CW) {
+                const int t2 = tt % B2, h = tt / B2;
             const int r2 = bin_to_tern(t2);
             uint32_t v[N1];
 #pragma unroll
             for (int x = 0; x < N1; x++) v[x] = 0;
 #pragma unroll
-            for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * 32 + lane];
+            for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * PITCH + 32 * h + lane];
             cube_merge<R1>(v);
             if (R2 == 0) cube_reduce_par<R1>(v);
 #pragma unroll
-            for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * 32 + lane] = v[x];
+            for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * PITCH + 32 * h + lane] = v[x];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&stage_free[b]);
         if (R2 > 0) {
             bar_compute(NCT);
-            for (int t1 = warp; t1 < N1; t1 += CW) {
+            for (int tt = warp; tt < N1 * CC; tt += CW) {
+                const int t1 = tt % N1, h = tt / N1;
                 uint32_t v[N2];
 #pragma unroll
                 for (int x = 0; x < N2; x++) v[x] = 0;
 #pragma unroll
-                for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * 32 + lane];
+                for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * PITCH + 32 * h + lane];
                 cube_merge<R2>(v);
                 cube_reduce_par<R2>(v);
 #pragma unroll
-                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * 32 + lane] = v[x];
+                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
             }
             bar_compute(NCT);
-            for (int t2 = warp; t2 < N2; t2 += CW) {
+            for (int tt = warp; tt < N2 * CC; tt += CW) {
+                const int t2 = tt % N2, h = tt / N2;
                 uint32_t v[N1];
 #pragma unroll
-                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * 32 + lane];
+                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
                 cube_reduce_par<R1>(v);
 #pragma unroll
-                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * 32 + lane] = v[x];
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
             }
         }
         if (ib_mask) {
@@ -1151,7 +1174,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            for (int t = threadIdx.x; t < NR * kRowBlocks; t += NCT) {
+            for (int t = threadIdx.x; t < NR * kRowBlocks * CC; t += NCT) {
                 uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
                 const uint4 x0 = p[0], x1 = p[1];
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
@@ -1456,7 +1479,7 @@ struct Timer {
 // 3-D tensor map over the state for a strided group: dim0 = words of the
 // inner extent (8*Q), dim1 = the 3^R rows (stride Q blocks), dim2 = outer
 // index (stride 3^R*Q blocks); box = 32 words x BOXR rows x 1.
-int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr) {
+int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr, int box0 = 32) {
     if (!g_eng.encode) {
         cudaDriverEntryPointQueryResult q;
         void *fn = nullptr;
@@ -1466,7 +1489,7 @@ int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t
     }
     cuuint64_t dims[3] = {(cuuint64_t)(8 * Q), (cuuint64_t)nr, (cuuint64_t)nouter};
     cuuint64_t strides[2] = {(cuuint64_t)(Q * 32), (cuuint64_t)(Q * 32 * nr)};
-    cuuint32_t box[3] = {32, (cuuint32_t)boxr, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)boxr, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = g_eng.encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, state, dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1477,13 +1500,13 @@ int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t
 
 // 5-D map for the binary-row gather of a MERGE_REDUCE group: dims {8Q words,
 // 3 x R1 digit dims (strides Q, 3Q, 9Q blocks), 3^R2}; box {32, 2, .., 2, 1}.
-int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2) {
+int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2, int box0 = 32) {
     cuuint64_t dims[5];
     cuuint64_t strides[4];
     cuuint32_t box[5], es[5];
     int rank = 0;
     dims[rank] = (cuuint64_t)(8 * Q);
-    box[rank] = 32;
+    box[rank] = (cuuint32_t)box0;
     es[rank++] = 1;
     int64_t st = Q * 32;
     for (int k = 0; k < r1; k++) {
@@ -1513,20 +1536,22 @@ int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2
 template <int R1, int R2, int MODE>
 int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
     using SM = PipeSmem<R1, R2>;
+    constexpr int CC = pipe_cols<R1, R2>();  // 128-B columns per tile
     CUtensorMap map, gmap;
     int rc;
-    if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR))) return rc;
+    if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR, 32 * CC))) return rc;
     if (MODE == MERGE_REDUCE) {
-        if ((rc = make_gather_map(&gmap, state, Q, R1, R2))) return rc;
+        if ((rc = make_gather_map(&gmap, state, Q, R1, R2, 32 * CC))) return rc;
     } else {
         gmap = map;
     }
-    const int64_t nitems = ncol * nouter;
+    const int64_t ncolg = (ncol + CC - 1) / CC;  // column groups: one tile each per outer index
+    const int64_t nitems = ncolg * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
-        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
+        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib);
     else
-        k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncol, nitems, ib);
+        k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib);
     CK(cudaGetLastError());
     return DQMC_OK;
 }
