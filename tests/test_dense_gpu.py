@@ -78,8 +78,12 @@ class TestSweeps:
             want = oracle_mod.dense_prime_ranks(w, n)
             assert np.array_equal(got, want), (n, d)
 
-    @pytest.mark.parametrize("n,p_on,p_dc", [(21, 0.75, 0.05), (22, 0.9, 0.05)])
+    @pytest.mark.parametrize(
+        "n,p_on,p_dc",
+        [(21, 0.75, 0.05), (22, 0.9, 0.05), pytest.param(23, 0.6, 0.1, marks=pytest.mark.slow)],
+    )
     def test_vs_oracle_large(self, pkg, oracle_mod, gen_mod, n, p_on, p_dc):
+        # n=21/22/23: groups (5,4)/(5,5)/(6,5): 3- and 8-column tiles in the strided passes
         v = gen_mod.gen3(n, p_on, p_dc, 3)
         got = pkg.prime_ranks_from_values(v)
         want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
