@@ -5,17 +5,21 @@
 // Design: the 3^(n-5) blocks of the reference layout are
 // swept in a handful of HBM passes instead of the reference's 2(n-5)+1:
 //
-//   pass A  k_c0_merge   : truth table -> blocks, in-block MERGE + the C0
-//                          block axes (contiguous 3^g-block tiles in smem);
-//                          only top-binary tiles are produced.
-//   pass B  k_strided<MERGE_ONLY>  : one group of <= 6 higher block axes,
-//                          reads the group's binary rows, writes its star rows.
-//   pass C  k_strided<MERGE_REDUCE>: last group: MERGE then REDUCE of the
-//                          group (+ some in-block axes); writes every block.
-//   pass D  k_strided<REDUCE>      : REDUCE of the remaining groups.
-//   pass E  k_c0_final   : REDUCE of the C0 axes + remaining in-block axes,
-//                          warp-aggregated popcount, decoupled look-back scan
-//                          and ordered compaction to int64 ranks.
+//   pass A  k_c0_merge          : truth table -> blocks, in-block MERGE + the C0
+//                                 block axes (contiguous 3^g-block tiles in smem);
+//                                 only top-binary tiles are produced.
+//   pass B  k_strided<MERGE_ONLY>: one group of <= 6 higher block axes, reads the
+//                                 group's binary rows, writes its star rows.
+//   pass C  k_merge_reduce_pipe  : last group: MERGE then REDUCE of the group
+//                                 (+ an in-block axis); TMA gather of the binary
+//                                 rows, TMA stores of every row (load / compute /
+//                                 store warps).
+//   pass D  k_strided_pipe<REDUCE_ONLY>: REDUCE of the other groups + 4 in-block
+//                                 axes; TMA tiles, one producer warp.
+//   pass E  k_c0_final           : REDUCE of the C0 axes, popcounts, per-tile
+//                                 scratch reservation and ordered compaction;
+//                                 then a CUB scan + k_reorder place the ranks.
+// Groups under 6 axes pack several adjacent 128-B columns per tile (pipe_cols).
 // Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -804,11 +808,11 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined strided pass (MERGE_REDUCE / REDUCE_ONLY): persistent CTAs, two
-// tile buffers, one producer warp that streams tiles in and out with TMA
-// (3-D tensor map: words x rows x outer; zero-fill / clipping handle the
-// ragged last column) while nine compute warps work on the other buffer.
-// MERGE_REDUCE gathers only the 2^R binary rows (cp.async, 16 B each).
+// Pipelined strided pass D (REDUCE_ONLY): persistent CTAs, two tile buffers,
+// one producer warp that streams tiles in and out with TMA (3-D tensor map:
+// words x rows x outer; zero-fill / clipping handle the ragged last column
+// group) while the compute warps work on the other buffer. Pass C
+// (k_merge_reduce_pipe, below) gathers only the 2^R binary rows.
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *mbar) {
     asm volatile(
@@ -929,30 +933,18 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 if (i < L) {
                     const int64_t it = item(i);
                     const int c0 = (int)((it % ncol) * 32 * CC), outer = (int)(it / ncol);
-                    if (MODE == REDUCE_ONLY) {
-                        // each box is reloaded as soon as its store has read it out of
-                        // smem: the next tile's load overlaps the previous tile's store
-                        mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
-                        static_assert(SM::NBOX <= 3, "box-wise store/load overlap handles <= 3 boxes");
+                    // each box is reloaded as soon as its store has read it out of
+                    // smem: the next tile's load overlaps the previous tile's store
+                    mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
+                    static_assert(SM::NBOX <= 3, "box-wise store/load overlap handles <= 3 boxes");
 #pragma unroll
-                        for (int x = 0; x < SM::NBOX; x++) {
-                            if (st) {
-                                if (SM::NBOX - 1 - x == 2) bulk_wait_read<2>();
-                                else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
-                                else bulk_wait_read<0>();
-                            }
-                            tma_load_3d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, outer, &full[b]);
+                    for (int x = 0; x < SM::NBOX; x++) {
+                        if (st) {
+                            if (SM::NBOX - 1 - x == 2) bulk_wait_read<2>();
+                            else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
+                            else bulk_wait_read<0>();
                         }
-                    } else {
-                        // binary rows: one 5-D box {32 words, 2, .., 2} per binary rho2; the
-                        // compute warps rewrite tile b once these land, so the store of the
-                        // previous tile in b must have read it out first
-                        if (st) bulk_wait_read<0>();
-                        uint32_t *stg = smem + 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
-                        mbar_expect_tx(&full[b], SM::STAGE_WORDS * 4);
-#pragma unroll
-                        for (int b2 = 0; b2 < B2; b2++)
-                            tma_load_5d(stg + b2 * B1 * PITCH, &gmap, c0, 0, 0, 0, bin_to_tern(b2), &full[b]);
+                        tma_load_3d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, outer, &full[b]);
                     }
                 }
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
@@ -968,80 +960,33 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
         const int b = (int)(i & 1);
         const int tb = b * SM::TILE_WORDS;
         mbar_wait(&full[b], (unsigned)((i >> 1) & 1));
-        if (MODE == MERGE_REDUCE) {
-            const int sb = 2 * SM::TILE_WORDS + b * SM::STAGE_WORDS;
-            // round 1: merge the R1 axes for each binary rho2
-            for (int tt = warp; tt < B2 * CC; tt += CW) {
-                const int t2 = tt % B2, h = tt / B2;
-                const int r2 = bin_to_tern(t2);
-                uint32_t v[N1];
+        // round 1: reduce the R1 axes
+        for (int tt = warp; tt < N2 * CC; tt += CW) {
+            const int t2 = tt % N2, h = tt / N2;
+            uint32_t v[N1];
 #pragma unroll
-                for (int x = 0; x < N1; x++) v[x] = 0;
+            for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
+            cube_reduce_par<R1>(v);
 #pragma unroll
-                for (int b1 = 0; b1 < B1; b1++) v[bin_to_tern(b1)] = smem[sb + (b1 + B1 * t2) * PITCH + 32 * h + lane];
-                cube_merge<R1>(v);
-                if (R2 == 0) cube_reduce_par<R1>(v);
-#pragma unroll
-                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * r2) * PITCH + 32 * h + lane] = v[x];
-            }
-            if (R2 > 0) {
-                bar_compute(NCT);
-                // round 2: merge + reduce the R2 axes
-                for (int tt = warp; tt < N1 * CC; tt += CW) {
+            for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
+        }
+        if (R2 > 0) {
+            bar_compute(NCT);
+            for (int tt = warp; tt < N1 * CC; tt += CW) {
                 const int t1 = tt % N1, h = tt / N1;
-                    uint32_t v[N2];
+                uint32_t v[N2];
 #pragma unroll
-                    for (int x = 0; x < N2; x++) v[x] = 0;
+                for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane];
+                cube_reduce_par<R2>(v);
 #pragma unroll
-                    for (int b2 = 0; b2 < B2; b2++) v[bin_to_tern(b2)] = smem[tb + (t1 + N1 * bin_to_tern(b2)) * PITCH + 32 * h + lane];
-                    cube_merge<R2>(v);
-                    cube_reduce_par<R2>(v);
-#pragma unroll
-                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
-                }
-                bar_compute(NCT);
-                // round 3: reduce the R1 axes
-                for (int tt = warp; tt < N2 * CC; tt += CW) {
-                const int t2 = tt % N2, h = tt / N2;
-                    uint32_t v[N1];
-#pragma unroll
-                    for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
-                    cube_reduce_par<R1>(v);
-#pragma unroll
-                    for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
-                }
-            }
-        } else {
-            // round 1: reduce the R1 axes
-            for (int tt = warp; tt < N2 * CC; tt += CW) {
-                const int t2 = tt % N2, h = tt / N2;
-                uint32_t v[N1];
-#pragma unroll
-                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
-                cube_reduce_par<R1>(v);
-#pragma unroll
-                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
-            }
-            if (R2 > 0) {
-                bar_compute(NCT);
-                for (int tt = warp; tt < N1 * CC; tt += CW) {
-                const int t1 = tt % N1, h = tt / N1;
-                    uint32_t v[N2];
-#pragma unroll
-                    for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane];
-                    cube_reduce_par<R2>(v);
-#pragma unroll
-                    for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
-                }
+                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
             }
         }
         if (ib_mask) {
             bar_compute(NCT);
-            // in-block axes, thread per block; halves swapped on lanes 4-7 of
-            // every 8 so each LDS.128/STS.128 quarter-warp hits 32 distinct banks
-            // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
-            // MIO wavefronts, which have slack here; a lane half-swap would cost
-            // 16 ALU selects per block on the saturated ALU pipe)
+            // in-block axes, thread per block; plain LDS.128 pairs (a 2-way bank
+            // conflict costs MIO wavefronts, which have slack here; a lane
+            // half-swap would cost 16 ALU selects per block on the saturated ALU pipe)
             for (int t = threadIdx.x; t < NR * kRowBlocks * CC; t += NCT) {
                 uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
                 const uint4 x0 = p[0], x1 = p[1];
@@ -1416,11 +1361,8 @@ int ensure_attrs() {
     CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     int rc;
-    if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;
-    if ((rc = set_mode_attrs<MERGE_REDUCE>())) return rc;
-    if ((rc = set_mode_attrs<REDUCE_ONLY>())) return rc;
-    if ((rc = set_pipe_attrs<MERGE_REDUCE>())) return rc;
-    if ((rc = set_pipe_attrs<REDUCE_ONLY>())) return rc;
+    if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;  // pass B (k_strided)
+    if ((rc = set_pipe_attrs<REDUCE_ONLY>())) return rc;  // pass D (k_strided_pipe)
     if ((rc = set_mr_attr<1, 0>()) || (rc = set_mr_attr<2, 0>()) || (rc = set_mr_attr<3, 0>()) ||
         (rc = set_mr_attr<2, 2>()) || (rc = set_mr_attr<3, 2>()) || (rc = set_mr_attr<3, 3>()))
         return rc;
