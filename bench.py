@@ -351,6 +351,7 @@ def run_engine_bench(args):
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": achieved / peak,
+            "frac_of_nominal_8000_gbs": achieved / 8000.0,  # also vs the 8 TB/s nominal
             "traffic": traffic,
             "algorithmic_bytes_per_launch": pass_bytes[dom],
             "ms_per_launch": dom_ms,
