@@ -379,14 +379,20 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
         const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
         int64_t *o = fa.out + pos;
         if (pos + cnt <= fa.cap) {
-            // the block as four 64-bit words: half the loops of a 32-bit walk
+            // walk only the nonzero words (most blocks hold one or two): their
+            // mask from the registers, the words themselves re-read from smem
+            uint32_t nz = 0;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                uint64_t w = ((uint64_t)wv[2 * k + 1] << 32) | wv[2 * k];
-                while (w) {
-                    *o++ = rbase + k * 64 + (__ffsll((long long)w) - 1);
+            for (int k = 0; k < 8; k++) nz |= (wv[k] != 0u ? 1u : 0u) << k;
+            const uint32_t *bw = sm + b * 8;
+            while (nz) {
+                const int k = __ffs(nz) - 1;
+                nz &= nz - 1;
+                uint32_t w = bw[k];
+                do {
+                    *o++ = rbase + k * 32 + (__ffs(w) - 1);
                     w &= w - 1;
-                }
+                } while (w);
             }
         } else {  // the scratch is too small: write what fits (the host grows it and reruns)
 #pragma unroll
