@@ -212,6 +212,7 @@ struct FinalArgs {
     int32_t *tile_cnt;          // per tile: prime count
     int64_t tile0;              // first tile of this launch (chunked final stage)
     int prefetch = 0;           // L2 prefetch distance in tiles (0: off)
+    int64_t pitch = 0;          // storage blocks per tile (0: 3^G, the reference layout)
 };
 
 
@@ -616,19 +617,18 @@ __device__ void tile_build(uint32_t *sm, const uint32_t *__restrict__ tt32, int 
 
 // pass A: top-binary tiles (2^T of them), merged over in-block + C0 axes
 __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__restrict__ tt32,
-                                                           uint32_t *__restrict__ state, int g, int T) {
+                                                           uint32_t *__restrict__ state, int g, int T, int pitch) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int64_t ntiles = 1ll << T;
     const int nb = (int)pow3l(g);
-    const int64_t p3g = pow3l(g);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int64_t base = 0, p = p3g;
+        int64_t base = 0, p = pitch;  // storage block of the tile: ternary index of its top digits x pitch
         for (int k = 0; k < T; k++, p *= 3)
             if ((tile >> k) & 1) base += p;
         tile_build(sm, tt32, g, tile);
         uint4 *dst = reinterpret_cast<uint4 *>(state + base * 8);
         const uint4 *src = reinterpret_cast<const uint4 *>(sm);
-        for (int t = threadIdx.x; t < nb * 2; t += blockDim.x) dst[t] = src[t];
+        for (int t = threadIdx.x; t < pitch * 2; t += blockDim.x) dst[t] = t < nb * 2 ? src[t] : make_uint4(0, 0, 0, 0);
         __syncthreads();
     }
 }
@@ -641,16 +641,18 @@ __global__ void __launch_bounds__(kFinalThreads, 3) k_c0_final(const uint32_t *_
     __shared__ __align__(8) uint64_t mbar;
     constexpr int NB = pow3i(G);
     const int64_t tile = blockIdx.x + fa.tile0;
-    const int64_t blk0 = tile * NB;
+    const int64_t blk0 = tile * NB;  // logical (rank) block
+    const int64_t pitch = fa.pitch ? fa.pitch : NB;
+    const uint32_t *src = state + tile * pitch * 8;
     if (threadIdx.x == 0) {
         mbar_init(&mbar, 1);
         mbar_expect_tx(&mbar, NB * 32);
-        bulk_g2s(sm, state + blk0 * 8, NB * 32, &mbar);
+        bulk_g2s(sm, src, NB * 32, &mbar);
         // warm L2 for the CTA that will take this slot a generation later
         // (CTAs start roughly in tile order, ~3 per SM resident)
         const int pf = (int)blockIdx.x + fa.prefetch;
         if (fa.prefetch > 0 && pf < (int)gridDim.x)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(state + (blk0 + (int64_t)fa.prefetch * NB) * 8),
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (int64_t)fa.prefetch * pitch * 8),
                          "r"(NB * 32)
                          : "memory");
     }
@@ -1158,9 +1160,18 @@ struct Plan {
     uint32_t ib_C = 0, ib_E = 0, ib_D[8] = {0};
     int64_t rank_sub = 0;
     int64_t nblocks = 0;
+    int64_t pitch = 0;   // storage blocks per C0 tile (3^g, or 3^g rounded up to 128 B)
+    uint64_t sbytes = 0; // storage bytes of the state
 };
 
-Plan make_plan(int n) {
+// padded: each C0 tile of 3^g blocks is stored at a pitch rounded up to a
+// multiple of 4 blocks (128 B; 2187 -> 2188 blocks at g = 7) so that every
+// 128-B row piece the strided passes move is 128-B aligned (TMA load+store of
+// misaligned 32-B-granular rows measured 24% slower, tools/probes/layout_probe.cu).
+// The pad block is zero and stays zero (MERGE: 0 & 0, REDUCE: 0 & ~x). Only the
+// fused single-GPU plan uses it; the bitmap-keeping and sharded entry points
+// keep the reference layout (dense.py:1-23).
+Plan make_plan(int n, bool padded = true) {
     Plan p;
     p.n = n;
     p.ne = n < 5 ? 5 : n;
@@ -1169,6 +1180,9 @@ Plan make_plan(int n) {
     p.g = std::min(p.H, kC0Max);
     p.T = p.H - p.g;
     p.nblocks = pow3l(p.H);
+    p.pitch = pow3l(p.g);
+    if (padded && p.T > 0) p.pitch = (p.pitch + kRowBlocks - 1) / kRowBlocks * kRowBlocks;
+    p.sbytes = (uint64_t)pow3l(p.T) * (uint64_t)p.pitch * 32;
     if (p.T > 0) {
         p.m = (p.T + kGroupMax - 1) / kGroupMax;
         int a = p.g;
@@ -1554,7 +1568,7 @@ void note_held(const Plan &p, bool keep);
 
 uint64_t engine_device_bytes(const Plan &p, bool keep) {
     if (p.T == 0 && !keep) return 0;
-    return (uint64_t)p.nblocks * 32 + (uint64_t)pow3l(p.T) * 20;
+    return p.sbytes + (uint64_t)pow3l(p.T) * 20;
 }
 
 int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArgs &fa, cudaStream_t s) {
@@ -1584,6 +1598,8 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
     if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    if ((kill || bitmap_out) && p.T > 0 && p.pitch != pow3l(p.g))
+        return set_err(DQMC_ERR_INVALID, "internal: kill/bitmap outputs need the reference layout plan");
     const bool direct = ntiles == 1;  // one tile: its ranks are already in order
     if (!count_only && !direct) {
         const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
@@ -1600,6 +1616,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
     fa.tile_base = g_eng.tile_base;
     fa.tile_cnt = g_eng.tile_cnt;
     fa.tile0 = 0;
+    fa.pitch = p.pitch;
     fa.prefetch = 3 * g_eng.num_sms;  // one generation of resident CTAs (3 per SM): 9.23 -> 9.0 ms at n=24
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
     if (tt32) {
@@ -1653,13 +1670,13 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
     const int tile_smem = (int)pow3l(p.g) * 32;
     const int64_t ntA = 1ll << p.T;
     const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
-    k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T);
+    k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T, p.pitch);
     CK(cudaGetLastError());
     tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
     auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
     const int last = full ? p.m : p.m - 1;
     for (int k = 0; k < last; k++) {
-        const int64_t Q = pow3l(p.a[k]);
+        const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
@@ -1680,7 +1697,7 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
     int rc;
     {
         const int k = p.m - 1;
-        const int64_t Q = pow3l(p.a[k]);
+        const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         if (fused) {
             if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
@@ -1691,7 +1708,7 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         }
     }
     for (int k = p.m - 2; k >= 0; k--) {
-        const int64_t Q = pow3l(p.a[k]);
+        const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
@@ -1742,7 +1759,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
     int rc;
     const uint64_t S = (uint64_t)p.nblocks * 32;
     if (p.T > 0 || keep) {
-        if ((rc = grow(g_eng.state, g_eng.state_cap, S, 1))) return rc;
+        if ((rc = grow(g_eng.state, g_eng.state_cap, std::max<uint64_t>(S, p.sbytes), 1))) return rc;
     }
     tm.begin();
     int64_t total = 0;
@@ -1788,7 +1805,7 @@ int input_words(const void *in, int kind, int n, const uint32_t **tt32, cudaStre
 // total device pass (input conversion + plan)
 int primes_device_impl(const void *in, int kind, int n, int64_t *ranks, int64_t cap, int64_t *count,
                        uint32_t flags, cudaStream_t s) {
-    const Plan p = make_plan(n);
+    const Plan p = make_plan(n, !(flags & DQMC_FLAG_KEEP_BITMAP));
     const uint32_t *tt32 = nullptr;
     int rc;
     if ((rc = input_words(in, kind, n, &tt32, s))) return rc;
@@ -1895,6 +1912,7 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
         fa.tile_base = g_eng.tile_base;
         fa.tile_cnt = g_eng.tile_cnt;
         fa.prefetch = 3 * g_eng.num_sms;
+        fa.pitch = p.pitch;
         CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
         CK(cudaMemsetAsync(g_eng.chunk_base, 0, 8, s));
         size_t tmp = 0;
@@ -1951,7 +1969,7 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
-    const Plan p = make_plan(n);
+    const Plan p = make_plan(n, !(flags & DQMC_FLAG_KEEP_BITMAP));
     if ((rc = check_cap(n, h, mem_cap, engine_device_bytes(p, flags & DQMC_FLAG_KEEP_BITMAP)))) return rc;
     cudaStream_t s = g_eng.stream;
     // H2D of the input (pageable source; small relative to the state)
@@ -1965,7 +1983,7 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
         // merge/reduce passes, then the chunked final stage straight into pinned host memory
         const uint32_t *tt32 = nullptr;
         if ((rc = input_words(g_eng.in_tmp, kind, n, &tt32, s))) return rc;
-        if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.nblocks * 32, 1))) return rc;
+        if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.sbytes, 1))) return rc;
         Timer tm{false, s};
         if ((rc = run_merge(p, tt32, g_eng.state, false, tm, s))) return rc;
         if ((rc = run_reduce(p, g_eng.state, true, tm, s))) return rc;
@@ -2050,7 +2068,7 @@ int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *j
             const size_t want = (size_t)((double)g_eng.hint_count * 1.05) + 4096;
             if ((rc = grow(g_eng.jranks[slot], g_eng.jranks_cap[slot], want, 8))) return rc;
             g_eng.scratch_want = std::max(g_eng.scratch_want, want);
-            if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.nblocks * 32, 1))) return rc;
+            if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.sbytes, 1))) return rc;
             cudaStream_t s = g_eng.stream;
             CK(cudaMemcpyAsync(g_eng.jin[slot], host_in, in_bytes, cudaMemcpyHostToDevice, s));
             const uint32_t *tt32 = nullptr;
@@ -2201,7 +2219,7 @@ int dqmc_primes_device(const void *input_dev, int in_kind, int n, int64_t *ranks
     std::lock_guard<std::mutex> lk(g_mu);
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
-    const Plan p = make_plan(n);
+    const Plan p = make_plan(n, !(flags & DQMC_FLAG_KEEP_BITMAP));
     if ((rc = check_cap(n, 0, 0, engine_device_bytes(p, flags & DQMC_FLAG_KEEP_BITMAP)))) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     if (!ranks_dev) flags |= DQMC_FLAG_COUNT_ONLY;
@@ -2225,7 +2243,7 @@ int dqmc_last_pass_bytes(uint64_t *bytes, int max) {
 
 int dqmc_bitmap_device(void **ptr, uint64_t *bytes) {
     if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
-    const Plan p = make_plan(g_eng.state_n);
+    const Plan p = make_plan(g_eng.state_n, false);
     if (ptr) *ptr = g_eng.state;
     if (bytes) *bytes = (uint64_t)p.nblocks * 32;
     return DQMC_OK;
@@ -2233,7 +2251,7 @@ int dqmc_bitmap_device(void **ptr, uint64_t *bytes) {
 
 int dqmc_bitmap_download(void *host, uint64_t bytes) {
     if (g_eng.state_n < 0) return set_err(DQMC_ERR_INVALID, "no bitmap held: run with DQMC_FLAG_KEEP_BITMAP");
-    const Plan p = make_plan(g_eng.state_n);
+    const Plan p = make_plan(g_eng.state_n, false);
     const uint64_t need = (uint64_t)p.nblocks * 32;
     if (bytes < need) return set_err(DQMC_ERR_INVALID, "host buffer too small");
     CK(cudaMemcpy(host, g_eng.state, need, cudaMemcpyDeviceToHost));
@@ -2400,7 +2418,7 @@ int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
-    const Plan p = make_plan(n);
+    const Plan p = make_plan(n, false);  // caller-owned state in the reference layout
     const uint32_t *tt32 = nullptr;
     if ((rc = input_words(input_dev, in_kind, n, &tt32, s))) return rc;
     Timer tm{false, s};
@@ -2419,7 +2437,7 @@ int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int
     if ((rc = ensure_device())) return rc;
     if ((rc = ensure_attrs())) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
-    const Plan p = make_plan(n);
+    const Plan p = make_plan(n, false);  // caller-owned state in the reference layout
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0 || ranks_dev == nullptr;
     Timer tm{(flags & DQMC_FLAG_TIMING) != 0, s};
     tm.begin();
