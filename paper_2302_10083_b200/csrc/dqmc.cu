@@ -213,6 +213,8 @@ struct FinalArgs {
     int64_t tile0;              // first tile of this launch (chunked final stage)
     int prefetch = 0;           // L2 prefetch distance in tiles (0: off)
     int64_t pitch = 0;          // storage blocks per tile (0: 3^G, the reference layout)
+    int pm_nr = 0;              // piece-major group 0 (make_plan): its 3^r rows; 0 = contiguous tiles
+    int pm_np = 0;              // pieces (128 B) per tile
 };
 
 
@@ -617,7 +619,8 @@ __device__ void tile_build(uint32_t *sm, const uint32_t *__restrict__ tt32, int 
 
 // pass A: top-binary tiles (2^T of them), merged over in-block + C0 axes
 __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__restrict__ tt32,
-                                                           uint32_t *__restrict__ state, int g, int T, int pitch) {
+                                                           uint32_t *__restrict__ state, int g, int T, int pitch,
+                                                           int pm_r) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int64_t ntiles = 1ll << T;
     const int nb = (int)pow3l(g);
@@ -626,25 +629,61 @@ __global__ void __launch_bounds__(kTileThreads) k_c0_merge(const uint32_t *__res
         for (int k = 0; k < T; k++, p *= 3)
             if ((tile >> k) & 1) base += p;
         tile_build(sm, tt32, g, tile);
-        uint4 *dst = reinterpret_cast<uint4 *>(state + base * 8);
         const uint4 *src = reinterpret_cast<const uint4 *>(sm);
-        for (int t = threadIdx.x; t < pitch * 2; t += blockDim.x) dst[t] = t < nb * 2 ? src[t] : make_uint4(0, 0, 0, 0);
+        if (pm_r) {
+            // piece-major group 0 (make_plan): piece x of the tile lives at
+            // ((upper * npieces + x) * 3^r + row0) pieces, row0 = the group-0 digits
+            const int64_t nr = pow3l(pm_r), np = pitch / kRowBlocks;
+            const int64_t row0 = (int64_t)bin_to_tern_rt((uint64_t)(tile & ((1ll << pm_r) - 1)));
+            const int64_t upper = (int64_t)bin_to_tern_rt((uint64_t)(tile >> pm_r));
+            uint4 *dst = reinterpret_cast<uint4 *>(state) + ((upper * np) * nr + row0) * 8;
+            for (int t = threadIdx.x; t < pitch * 2; t += blockDim.x)
+                dst[(int64_t)(t >> 3) * nr * 8 + (t & 7)] = t < nb * 2 ? src[t] : make_uint4(0, 0, 0, 0);
+        } else {
+            uint4 *dst = reinterpret_cast<uint4 *>(state + base * 8);
+            for (int t = threadIdx.x; t < pitch * 2; t += blockDim.x) dst[t] = t < nb * 2 ? src[t] : make_uint4(0, 0, 0, 0);
+        }
         __syncthreads();
     }
 }
 
 // pass E: one CTA per C0 tile (3^G blocks), tiles taken in rank order by
 // ticket; the tile arrives in shared memory with one TMA bulk copy.
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *mbar);
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap *map, int c0, int c1, int c2, int c3);
+
 template <int G>
-__global__ void __launch_bounds__(kFinalThreads, 3) k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa) {
-    extern __shared__ __align__(128) uint32_t sm[];
+__global__ void __launch_bounds__(kFinalThreads, 3)
+    k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa, const __grid_constant__ CUtensorMap ma,
+               const __grid_constant__ CUtensorMap mb) {
+    extern __shared__ __align__(128) uint32_t sm_raw[];
     __shared__ __align__(8) uint64_t mbar;
     constexpr int NB = pow3i(G);
+    // tensor-map destinations need 128-B alignment; the dynamic window follows
+    // this kernel's static arrays (the launch reserves 128 B for the shift)
+    uint32_t *sm = sm_raw + (fa.pm_nr ? ((128u - (smem_u32(sm_raw) & 127u)) & 127u) >> 2 : 0u);
     const int64_t tile = blockIdx.x + fa.tile0;
     const int64_t blk0 = tile * NB;  // logical (rank) block
     const int64_t pitch = fa.pitch ? fa.pitch : NB;
     const uint32_t *src = state + tile * pitch * 8;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && fa.pm_nr) {
+        // piece-major group 0: the tile is pm_np pieces 3^r pieces apart; boxes
+        // of 256 pieces (map ma) and one remainder box (map mb)
+        mbar_init(&mbar, 1);
+        mbar_expect_tx(&mbar, fa.pm_np * 128);
+        const int nfull = fa.pm_np >> 8, rem = fa.pm_np & 255;
+        const int q1 = (int)(tile % fa.pm_nr), up = (int)(tile / fa.pm_nr);
+        for (int j = 0; j < nfull; j++) tma_load_4d(sm + j * 256 * 32, &ma, 0, 256 * j, q1, up, &mbar);
+        if (rem) tma_load_4d(sm + nfull * 256 * 32, &mb, 0, 256 * nfull, q1, up, &mbar);
+        const int pf = (int)blockIdx.x + fa.prefetch;
+        if (fa.prefetch > 0 && pf < (int)gridDim.x) {
+            const int64_t t2 = tile + fa.prefetch;
+            const int q1b = (int)(t2 % fa.pm_nr), upb = (int)(t2 / fa.pm_nr);
+            for (int j = 0; j < nfull; j++) tma_prefetch_4d(&ma, 0, 256 * j, q1b, upb);
+            if (rem) tma_prefetch_4d(&mb, 0, 256 * nfull, q1b, upb);
+        }
+    } else if (threadIdx.x == 0) {
         mbar_init(&mbar, 1);
         mbar_expect_tx(&mbar, NB * 32);
         bulk_g2s(sm, src, NB * 32, &mbar);
@@ -677,13 +716,16 @@ __global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restri
 
 template <int R1, int R2, int MODE>
 __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restrict__ state, int64_t Q, int64_t ncol,
-                                                             int64_t nitems, uint32_t ib_mask) {
+                                                             int64_t nitems, uint32_t ib_mask, int64_t rs, int64_t cs,
+                                                             int64_t os) {
     constexpr int N1 = P3<R1>::v, N2 = P3<R2>::v, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = N1 * N2;
     extern __shared__ __align__(16) uint32_t sm[];  // NR rows x 32 words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
-    const int64_t Qw = Q * 8;  // row stride in words
+    // strides in blocks: row rs, column cs, outer os (reference layout: Q, 4,
+    // 3^R Q; piece-major group 0: 4, 3^R 4, pitch 3^R)
+    const int64_t Qw = rs * 8;  // row stride in words
 
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         const int64_t col = item % ncol;
@@ -692,7 +734,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
         const int64_t c0 = col * kRowBlocks;
         const int valid = (int)min((int64_t)kRowBlocks, Q - c0) * 8;
         const bool act = lane < valid;
-        uint32_t *g0 = state + (ob * NR * Q + c0) * 8 + lane;  // word of row 0
+        uint32_t *g0 = state + (ob * os + col * cs) * 8 + lane;  // word of row 0
         // in-block round needed?
         const bool ib = (MODE != MERGE_ONLY) && ib_mask != 0;
 
@@ -814,7 +856,7 @@ __global__ void __launch_bounds__(kStridedThreads) k_strided(uint32_t *__restric
                 const uint4 x0 = p[0], x1 = p[1];
                 uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
                 inblock_reduce(v, ib_mask);
-                uint4 *q = reinterpret_cast<uint4 *>(state + (ob * NR * Q + (int64_t)row * Q + c0 + b) * 8);
+                uint4 *q = reinterpret_cast<uint4 *>(state + (ob * os + (int64_t)row * rs + col * cs + b) * 8);
                 q[0] = make_uint4(v[0], v[1], v[2], v[3]);
                 q[1] = make_uint4(v[4], v[5], v[6], v[7]);
             }
@@ -841,6 +883,27 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int c1, int c2, const void *src) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
                  "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, int c0, int c1, int c2, int c3, const void *src) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap *map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),
+                 "r"(c2), "r"(c3)
                  : "memory");
 }
 
@@ -904,10 +967,44 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
+// At n = 24 about four in five blocks of the state are zero (a block is
+// nonzero only when its 19 block digits hold few stars: M(c) = AND over 2^stars
+// completions), and reducing a zero cell is a no-op. Sparse mode skips the
+// REDUCE work of a warp whose words are all zero (one vote per task).
+template <int N>
+__device__ __forceinline__ bool warp_any(const uint32_t (&v)[N]) {
+    uint32_t a = 0;
+#pragma unroll
+    for (int x = 0; x < N; x++) a |= v[x];
+    return __any_sync(0xffffffffu, a != 0u);
+}
+
+// In-block REDUCE of a smem tile, thread per 32-B block (plain LDS.128 pairs:
+// a 2-way bank conflict costs MIO wavefronts, which have slack, where a lane
+// half-swap would cost 16 ALU selects per block). Warp-uniform iterations so
+// an all-zero warp can skip (sparse).
+__device__ __forceinline__ void inblock_round(uint32_t *tile, int nblocks, uint32_t ib_mask, int nct, int sparse) {
+    const int lane = threadIdx.x & 31;
+    for (int t0 = (int)(threadIdx.x & ~31u); t0 < nblocks; t0 += nct) {
+        const int t = t0 + lane;
+        const bool in = t < nblocks;
+        uint4 *p = reinterpret_cast<uint4 *>(tile + (in ? t : 0) * 8);
+        uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+        if (in) x0 = p[0], x1 = p[1];
+        if (sparse && !__any_sync(0xffffffffu, (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u)) continue;
+        uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        inblock_reduce(v, ib_mask);
+        if (in) {
+            p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+        }
+    }
+}
+
 template <int R1, int R2, int MODE>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
-                   int64_t ncol, int64_t nitems, uint32_t ib_mask) {
+                   int64_t ncol, int64_t nitems, uint32_t ib_mask, int pm, int sparse) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
@@ -915,6 +1012,14 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t full[2], computed[2];
+    // 4-D map coordinates of an item: reference layout {col words, row, outer, 0};
+    // piece-major group 0 (pm, CC = 1) {0, row, col, outer} (make_group_map4)
+    auto crd = [&](int64_t it, int &c0, int &c2, int &c3) {
+        const int64_t col = it % ncol, outer = it / ncol;
+        c0 = pm ? 0 : (int)(col * 32 * CC);
+        c2 = (int)(pm ? col : outer);
+        c3 = pm ? (int)outer : 0;
+    };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // items strided over the grid: the CTAs work on adjacent columns at the same
     // time (a contiguous range per CTA measured 16.0 vs 13.9 ms at n = 24)
@@ -939,16 +1044,18 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 if (st) {
                     const int64_t it = item(i - 2);
                     mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
-                    const int c0 = (int)((it % ncol) * 32 * CC), c2 = (int)(it / ncol);
+                    int c0, c2, c3;
+                    crd(it, c0, c2, c3);
 #pragma unroll
                     for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
-                        tma_store_3d(&tmap, c0, x * SM::BOXR, c2, tile + x * SM::BOXR * PITCH);
+                        tma_store_4d(&tmap, c0, x * SM::BOXR, c2, c3, tile + x * SM::BOXR * PITCH);
                         bulk_commit();
                     }
                 }
                 if (i < L) {
                     const int64_t it = item(i);
-                    const int c0 = (int)((it % ncol) * 32 * CC), outer = (int)(it / ncol);
+                    int c0, c2, c3;
+                    crd(it, c0, c2, c3);
                     // each box is reloaded as soon as its store has read it out of
                     // smem: the next tile's load overlaps the previous tile's store
                     mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
@@ -960,7 +1067,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                             else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
                             else bulk_wait_read<0>();
                         }
-                        tma_load_3d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, outer, &full[b]);
+                        tma_load_4d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, c2, c3, &full[b]);
                     }
                 }
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
@@ -982,6 +1089,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             uint32_t v[N1];
 #pragma unroll
             for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
+            if (sparse && !warp_any(v)) continue;
             cube_reduce_par<R1>(v);
 #pragma unroll
             for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
@@ -993,6 +1101,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 uint32_t v[N2];
 #pragma unroll
                 for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane];
+                if (sparse && !warp_any(v)) continue;
                 cube_reduce_par<R2>(v);
 #pragma unroll
                 for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
@@ -1003,14 +1112,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             // in-block axes, thread per block; plain LDS.128 pairs (a 2-way bank
             // conflict costs MIO wavefronts, which have slack here; a lane
             // half-swap would cost 16 ALU selects per block on the saturated ALU pipe)
-            for (int t = threadIdx.x; t < NR * kRowBlocks * CC; t += NCT) {
-                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
-                const uint4 x0 = p[0], x1 = p[1];
-                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                inblock_reduce(v, ib_mask);
-                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
-            }
+            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
         }
         fence_async_smem();
         __syncwarp();
@@ -1025,7 +1127,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
-                        int64_t ncol, int64_t nitems, uint32_t ib_mask) {
+                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
@@ -1125,6 +1227,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
                 uint32_t v[N1];
 #pragma unroll
                 for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
+                if (sparse && !warp_any(v)) continue;
                 cube_reduce_par<R1>(v);
 #pragma unroll
                 for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
@@ -1135,14 +1238,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            for (int t = threadIdx.x; t < NR * kRowBlocks * CC; t += NCT) {
-                uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + t * 8]);
-                const uint4 x0 = p[0], x1 = p[1];
-                uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                inblock_reduce(v, ib_mask);
-                p[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                p[1] = make_uint4(v[4], v[5], v[6], v[7]);
-            }
+            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
         }
         fence_async_smem();
         __syncwarp();
@@ -1162,6 +1258,7 @@ struct Plan {
     int64_t nblocks = 0;
     int64_t pitch = 0;   // storage blocks per C0 tile (3^g, or 3^g rounded up to 128 B)
     uint64_t sbytes = 0; // storage bytes of the state
+    bool pm = false;     // piece-major storage of group 0 (see make_plan)
 };
 
 // padded: each C0 tile of 3^g blocks is stored at a pitch rounded up to a
@@ -1193,22 +1290,40 @@ Plan make_plan(int n, bool padded = true) {
             a += rk;
         }
     }
+    // piece-major group 0: the state is stored as [upper digits][piece x of the
+    // C0 tile][group-0 row][128 B] instead of [upper][group-0 row][C0 tile], so
+    // the tile of pass D (group 0 reduce, the read+write pass) is one
+    // contiguous 93 KB range instead of 729 pieces 70 KB apart, and pass E reads
+    // its C0 tile as pieces 93 KB apart (tools/probes/layout_probe.cu: in-place
+    // R+W of contiguous tiles 11.8 vs 15.6 ms; the E read 5.9 vs 5.1 ms).
+    // Groups above 0 see the same rows/columns as before (columns enumerate the
+    // pieces). Needs one 128-B column per tile (3^6 rows) and a separate D pass.
+    p.pm = padded && p.T > 0 && p.m >= 2 && p.r[0] == kGroupMax && !getenv("DQMC_NO_PM");
     // distribute the five in-block REDUCE axes over the passes that hold whole
-    // blocks: pass C (write-only) takes 1, the read+write passes D share the
-    // rest (their HBM time leaves the most ALU slack), the final pass E takes
-    // none when a D pass exists (it is issue-bound by the C0 axes + compaction).
+    // blocks: pass C (write-only) takes axes 1 and 4, the read+write passes D
+    // share the rest, the final pass E takes none when a D pass exists (it is
+    // latency-bound by the C0 axes + compaction). With the sparse skip, D runs
+    // at the HBM copy rate with three axes (n = 24: C 9.8 / D 11.6 ms; axes
+    // 1 / 2-5 gave 10.8 / 12.5, 1-2 / 3-5 10.0 / 11.5, none / all 11.9 / 11.8
+    // — tools/ab_ib.sh).
     if (p.T == 0) {
         p.ib_E = 31u;
     } else if (p.m == 1) {
         p.ib_C = 3u;   // axes 1,2
         p.ib_E = 28u;  // axes 3,4,5
     } else {
-        p.ib_C = 1u;
-        int axis = 1;
+        p.ib_C = 9u;
+        const int rest[3] = {1, 2, 4};  // 0-based axes 2, 3, 5
+        int i = 0;
         const int nd = p.m - 1;
         for (int q = 0; q < nd; q++) {
-            const int take = (4 - (axis - 1)) / (nd - q);
-            for (int c = 0; c < take; c++) p.ib_D[p.m - 2 - q] |= 1u << axis++;
+            const int take = (3 - i) / (nd - q);
+            for (int c = 0; c < take; c++) p.ib_D[p.m - 2 - q] |= 1u << rest[i++];
+        }
+        if (const char *e = getenv("DQMC_IB_C")) {  // experiment: C's in-block axes; the first D pass takes the rest
+            p.ib_C = (uint32_t)strtoul(e, nullptr, 0) & 31u;
+            for (int k = 0; k < 8; k++) p.ib_D[k] = 0;
+            p.ib_D[p.m - 2] = 31u & ~p.ib_C;
         }
     }
     return p;
@@ -1216,6 +1331,7 @@ Plan make_plan(int n, bool padded = true) {
 
 thread_local std::string g_err;
 const bool g_debug = getenv("DQMC_DEBUG") != nullptr;  // sync + report after every pass
+const int g_sparse = getenv("DQMC_NO_SPARSE") ? 0 : 1;  // skip all-zero warps in the reduce rounds
 std::mutex g_mu;
 
 int set_err(int code, const std::string &msg) {
@@ -1386,7 +1502,8 @@ int ensure_attrs() {
     if (g_eng.attrs_set) return DQMC_OK;
     const int tile_smem = (int)pow3l(kC0Max) * 32;
     CK(cudaFuncSetAttribute(k_c0_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
-    CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    // + one 128-B piece (the padded pitch of a piece-major tile, make_plan) + 128 B of alignment
+    CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem + 256));
     CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     int rc;
     if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;  // pass B (k_strided)
@@ -1449,7 +1566,7 @@ struct Timer {
 // 3-D tensor map over the state for a strided group: dim0 = words of the
 // inner extent (8*Q), dim1 = the 3^R rows (stride Q blocks), dim2 = outer
 // index (stride 3^R*Q blocks); box = 32 words x BOXR rows x 1.
-int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr, int box0 = 32) {
+int ensure_encode() {
     if (!g_eng.encode) {
         cudaDriverEntryPointQueryResult q;
         void *fn = nullptr;
@@ -1457,6 +1574,12 @@ int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t
         if (!fn || q != cudaDriverEntryPointSuccess) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
         g_eng.encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
     }
+    return DQMC_OK;
+}
+
+int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr, int box0 = 32) {
+    int rc;
+    if ((rc = ensure_encode())) return rc;
     cuuint64_t dims[3] = {(cuuint64_t)(8 * Q), (cuuint64_t)nr, (cuuint64_t)nouter};
     cuuint64_t strides[2] = {(cuuint64_t)(Q * 32), (cuuint64_t)(Q * 32 * nr)};
     cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)boxr, 1};
@@ -1465,6 +1588,31 @@ int make_group_map(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return DQMC_OK;
+}
+
+// 4-D map for the reduce-only pipe: the reference layout as {8Q words, rows,
+// outer, 1}; piece-major group 0 (pm) as {32 words, rows (128 B apart),
+// columns (3^R pieces apart), outer (Q/4 * 3^R pieces apart)}.
+int make_group_map4(CUtensorMap *map, uint32_t *state, int64_t Q, int nr, int64_t nouter, int boxr, int box0, bool pm) {
+    int rc;
+    if ((rc = ensure_encode())) return rc;
+    cuuint64_t dims[4], strides[3];
+    if (pm) {
+        const int64_t ncol = Q / kRowBlocks;
+        dims[0] = 32, dims[1] = (cuuint64_t)nr, dims[2] = (cuuint64_t)ncol, dims[3] = (cuuint64_t)nouter;
+        strides[0] = 128, strides[1] = (cuuint64_t)nr * 128, strides[2] = (cuuint64_t)(ncol * nr * 128);
+    } else {
+        dims[0] = (cuuint64_t)(8 * Q), dims[1] = (cuuint64_t)nr, dims[2] = (cuuint64_t)nouter, dims[3] = 1;
+        strides[0] = (cuuint64_t)(Q * 32), strides[1] = (cuuint64_t)(Q * 32 * nr),
+        strides[2] = (cuuint64_t)(Q * 32 * nr * nouter);
+    }
+    cuuint32_t box[4] = {(cuuint32_t)box0, (cuuint32_t)boxr, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = g_eng.encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, state, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (4-D) failed: " + std::to_string((int)r));
     return DQMC_OK;
 }
 
@@ -1504,12 +1652,17 @@ int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2
 }
 
 template <int R1, int R2, int MODE>
-int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
+int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s) {
     using SM = PipeSmem<R1, R2>;
     constexpr int CC = pipe_cols<R1, R2>();  // 128-B columns per tile
     CUtensorMap map, gmap;
     int rc;
-    if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR, 32 * CC))) return rc;
+    if (pm && (CC != 1 || MODE == MERGE_REDUCE)) return set_err(DQMC_ERR_INVALID, "internal: piece-major needs CC = 1");
+    if (MODE == MERGE_REDUCE) {
+        if ((rc = make_group_map(&map, state, Q, SM::NR, nouter, SM::BOXR, 32 * CC))) return rc;
+    } else {
+        if ((rc = make_group_map4(&map, state, Q, SM::NR, nouter, SM::BOXR, 32 * CC, pm))) return rc;
+    }
     if (MODE == MERGE_REDUCE) {
         if ((rc = make_gather_map(&gmap, state, Q, R1, R2, 32 * CC))) return rc;
     } else {
@@ -1519,32 +1672,35 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     const int64_t nitems = ncolg * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
-        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib);
+        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, g_sparse);
     else
-        k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib);
+        k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, pm ? 1 : 0,
+                                                                          g_sparse);
     CK(cudaGetLastError());
     return DQMC_OK;
 }
 
 template <int MODE>
-int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s) {
+int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s,
+                     bool pm = false) {
     switch (r) {
-        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, s);
-        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, s);
-        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, s);
-        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, s);
-        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, s);
-        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, s);
+        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s);
     }
 }
 
 template <int MODE>
-void launch_strided_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nitems, uint32_t ib,
+void launch_strided_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nitems, uint32_t ib, bool pm,
                          cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(nitems, 148ll * 16);
 #define LS(R1, R2)                                                                             \
-    k_strided<R1, R2, MODE><<<grid, kStridedThreads, P3<R1>::v * P3<R2>::v * 32 * 4, s>>>(state, Q, ncol, \
-                                                                                        nitems, ib)
+    k_strided<R1, R2, MODE><<<grid, kStridedThreads, P3<R1>::v * P3<R2>::v * 32 * 4, s>>>(                 \
+        state, Q, ncol, nitems, ib, pm ? kRowBlocks : Q, pm ? P3<R1>::v * P3<R2>::v * kRowBlocks : kRowBlocks, \
+        pm ? Q * P3<R1>::v * P3<R2>::v : P3<R1>::v * P3<R2>::v * Q)
     switch (r) {
         case 1: LS(1, 0); break;
         case 2: LS(2, 0); break;
@@ -1571,12 +1727,41 @@ uint64_t engine_device_bytes(const Plan &p, bool keep) {
     return p.sbytes + (uint64_t)pow3l(p.T) * 20;
 }
 
-int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArgs &fa, cudaStream_t s) {
-    const int smem = (int)pow3l(g) * 32;
+// E's tensor maps for piece-major group 0: dims {32 words, pieces (3^r x 128 B
+// apart), group-0 rows (128 B apart), upper (pieces x 3^r x 128 B apart)}
+int make_final_maps(const Plan &p, const uint32_t *state, CUtensorMap *ma, CUtensorMap *mb, FinalArgs &fa) {
+    memset(ma, 0, sizeof *ma);
+    memset(mb, 0, sizeof *mb);
+    fa.pm_nr = 0;
+    fa.pm_np = 0;
+    if (!p.pm) return DQMC_OK;
+    int rc;
+    if ((rc = ensure_encode())) return rc;
+    const int64_t nr = pow3l(p.r[0]), np = p.pitch / kRowBlocks, nu = pow3l(p.T - p.r[0]);
+    cuuint64_t dims[4] = {32, (cuuint64_t)np, (cuuint64_t)nr, (cuuint64_t)nu};
+    cuuint64_t strides[3] = {(cuuint64_t)(nr * 128), 128, (cuuint64_t)(np * nr * 128)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    for (int k = 0; k < 2; k++) {
+        const int rows = k == 0 ? 256 : (int)(np & 255);
+        if (rows == 0) continue;
+        cuuint32_t box[4] = {32, (cuuint32_t)rows, 1, 1};
+        CUresult r = g_eng.encode(k == 0 ? ma : mb, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (void *)state, dims, strides, box,
+                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (final) failed: " + std::to_string((int)r));
+    }
+    fa.pm_nr = (int)nr;
+    fa.pm_np = (int)np;
+    return DQMC_OK;
+}
+
+int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArgs &fa, const CUtensorMap &ma,
+                    const CUtensorMap &mb, cudaStream_t s) {
+    const int smem = fa.pm_nr ? fa.pm_np * 128 + 128 : (int)pow3l(g) * 32;
     switch (g) {
 #define CASE(G)                                                                         \
     case G:                                                                             \
-        k_c0_final<G><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa);          \
+        k_c0_final<G><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);  \
         break;
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
@@ -1624,7 +1809,9 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, const 
         CK(cudaGetLastError());
         tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (bitmap_out ? S : 0));
     } else {
-        if ((rc = launch_c0_final(p.g, ntiles, state, fa, s))) return rc;
+        CUtensorMap ma, mb;
+        if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
+        if ((rc = launch_c0_final(p.g, ntiles, state, fa, ma, mb, s))) return rc;
         tm.mark("k_c0_final", S + (kill ? S : 0) + (bitmap_out ? S : 0));
     }
     if (ntiles <= 4096 || getenv("DQMC_NO_CUB")) {
@@ -1670,7 +1857,7 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
     const int tile_smem = (int)pow3l(p.g) * 32;
     const int64_t ntA = 1ll << p.T;
     const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
-    k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T, p.pitch);
+    k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T, p.pitch, p.pm ? p.r[0] : 0);
     CK(cudaGetLastError());
     tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
     auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
@@ -1681,7 +1868,7 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
         const int64_t nitems = ncol << above;
-        launch_strided_mode<MERGE_ONLY>(p.r[k], state, Q, ncol, nitems, 0, s);
+        launch_strided_mode<MERGE_ONLY>(p.r[k], state, Q, ncol, nitems, 0, k == 0 && p.pm, s);
         CK(cudaGetLastError());
         tm.mark("k_strided<MERGE_ONLY>", (uint64_t)frac(above));
     }
@@ -1712,7 +1899,8 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
-        if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above), p.ib_D[k], s))) return rc;
+        if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above), p.ib_D[k], s, k == 0 && p.pm)))
+            return rc;
         tm.mark("k_strided<REDUCE>", 2 * S);
     }
     return DQMC_OK;
@@ -1913,6 +2101,8 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
         fa.tile_cnt = g_eng.tile_cnt;
         fa.prefetch = 3 * g_eng.num_sms;
         fa.pitch = p.pitch;
+        CUtensorMap ma, mb;
+        if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
         CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
         CK(cudaMemsetAsync(g_eng.chunk_base, 0, 8, s));
         size_t tmp = 0;
@@ -1922,7 +2112,7 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
         for (int c = 0; c < K; c++) {
             const int64_t t0 = ntiles * c / K, t1 = ntiles * (c + 1) / K;
             fa.tile0 = t0;
-            if ((rc = launch_c0_final(p.g, t1 - t0, state, fa, s))) return rc;
+            if ((rc = launch_c0_final(p.g, t1 - t0, state, fa, ma, mb, s))) return rc;
             CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt + t0, g_eng.tile_pos + t0, cub::Sum(),
                                               (int64_t)0, (int)(t1 - t0), s));
             k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c,

@@ -154,5 +154,11 @@ int main() {
     run("contiguous copy", ct, ctb, Pat{1, items, cont, cont, 1, 1});
     const Side cont_x = {{0, 0, 1, 0}, {0, 0, X, 0}, {0, BOXR, 0, 0}};
     run("contiguous read -> L' far write (x fastest)", ct, lp, Pat{X, items, cont_x, lp_x_q2, 1, 1});
+    run("D new2: contiguous 93 KB tiles in place", ct, ct, Pat{1, items, cont, cont, 1, 1});
+    // E under layout [q2][x][q1][128B]: tile (q2, q1) = 547 pieces at stride TILE; dims {32, q1, x, q2}
+    CUtensorMap ex = mk(a, 32, Q, X, Q, 128, TILE, (uint64_t)X * TILE, 1, BOXR, 1);
+    const Side e_q1_q2 = {{0, 1, 0, 0}, {0, 0, 0, 1}, {0, 0, BOXR, 0}};
+    run("E new2: 547 pieces at 93 KB stride (read only)", ex, ex, Pat{Q, (int64_t)Q * Q, e_q1_q2, {}, 1, 0});
+    run("E now: contiguous 70 KB (read only, as 729-row box)", ct, ct, Pat{1, items, cont, {}, 1, 0});
     return 0;
 }
