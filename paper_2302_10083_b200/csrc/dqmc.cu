@@ -562,6 +562,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, unsigned phase) {
         : "memory");
 }
 
+// At n = 24 about four in five blocks of the state are zero (a block is
+// nonzero only when its 19 block digits hold few stars: M(c) = AND over 2^stars
+// completions), and reducing a zero cell is a no-op. The reduce rounds skip
+// the work of a warp whose words are all zero (one vote per task).
+template <int N>
+__device__ __forceinline__ bool warp_any(const uint32_t (&v)[N]) {
+    uint32_t a = 0;
+#pragma unroll
+    for (int x = 0; x < N; x++) a |= v[x];
+    return __any_sync(0xffffffffu, a != 0u);
+}
+
 // REDUCE along C0 axes [J0, J0+K) of a 3^G-block tile, compile-time shape.
 template <int K, int G, int J0>
 __device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
@@ -570,13 +582,21 @@ __device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
     constexpr int SPAN = SJ * N;
     constexpr int NHI = pow3i(G) / SPAN;
     constexpr int NTASK = SJ * NHI * 8;
-    for (int t = threadIdx.x; t < NTASK; t += blockDim.x) {
-        const int w = t & 7, q = t >> 3;
+    // warp-uniform iterations: an all-zero warp skips its reduce (see warp_any)
+    for (int t0 = (int)(threadIdx.x & ~31u); t0 < NTASK; t0 += blockDim.x) {
+        const int t = t0 + (int)(threadIdx.x & 31u);
+        const bool in = t < NTASK;
+        const int w = t & 7, q = in ? t >> 3 : 0;
         const int lo = q % SJ, hi = q / SJ;
         const int blk = lo + hi * SPAN;
         uint32_t v[N];
 #pragma unroll
         for (int i = 0; i < N; i++) v[i] = sm[(blk + i * SJ) * 8 + w];
+        if (K <= 3) {  // 81-register cubes (K = 4) would spill with the vote
+            if (!warp_any(v) || !in) continue;
+        } else if (!in) {
+            continue;
+        }
         cube_reduce_par<K>(v);
 #pragma unroll
         for (int i = 0; i < N; i++) sm[(blk + i * SJ) * 8 + w] = v[i];
@@ -967,17 +987,7 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
-// At n = 24 about four in five blocks of the state are zero (a block is
-// nonzero only when its 19 block digits hold few stars: M(c) = AND over 2^stars
-// completions), and reducing a zero cell is a no-op. Sparse mode skips the
-// REDUCE work of a warp whose words are all zero (one vote per task).
-template <int N>
-__device__ __forceinline__ bool warp_any(const uint32_t (&v)[N]) {
-    uint32_t a = 0;
-#pragma unroll
-    for (int x = 0; x < N; x++) a |= v[x];
-    return __any_sync(0xffffffffu, a != 0u);
-}
+// Sparse mode: see warp_any.
 
 // In-block REDUCE of a smem tile, thread per 32-B block (plain LDS.128 pairs:
 // a 2-way bank conflict costs MIO wavefronts, which have slack, where a lane
@@ -998,6 +1008,35 @@ __device__ __forceinline__ void inblock_round(uint32_t *tile, int nblocks, uint3
             p[0] = make_uint4(v[0], v[1], v[2], v[3]);
             p[1] = make_uint4(v[4], v[5], v[6], v[7]);
         }
+    }
+}
+
+// inblock_round that also records which 128-B rows (4 blocks) of a one-column
+// tile are nonzero afterwards: bit r of rowbits (smem, cleared by the caller).
+__device__ __forceinline__ void inblock_round_bits(uint32_t *tile, int nblocks, uint32_t ib_mask, int nct,
+                                                   uint32_t *rowbits) {
+    const int lane = threadIdx.x & 31;
+    for (int t0 = (int)(threadIdx.x & ~31u); t0 < nblocks; t0 += nct) {
+        const int t = t0 + lane;
+        const bool in = t < nblocks;
+        uint4 *p = reinterpret_cast<uint4 *>(tile + (in ? t : 0) * 8);
+        uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+        if (in) x0 = p[0], x1 = p[1];
+        if (!__any_sync(0xffffffffu, (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u)) continue;
+        uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        inblock_reduce(v, ib_mask);
+        if (in) {
+            p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+        }
+        const bool nz = (v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7]) != 0u;
+        const uint32_t m = __ballot_sync(0xffffffffu, in && nz);
+        // lanes 4j..4j+3 hold row t0/4 + j (t0 is a multiple of 32: 8 whole rows)
+        uint32_t rb = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) rb |= ((m >> (4 * j)) & 0xFu) ? (1u << j) : 0u;
+        const int r0 = t0 >> 2;  // multiple of 8
+        if (lane == 0 && rb) atomicOr(&rowbits[r0 >> 5], rb << (r0 & 31));
     }
 }
 
@@ -1127,7 +1166,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
-                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse) {
+                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse, uint32_t *__restrict__ nzmap) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
@@ -1135,9 +1174,11 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t stage_full[2], stage_free[2], tile_done[2], tile_free[2];
+    __shared__ uint32_t s_rowbits[2][24];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
+    if (threadIdx.x < 48) s_rowbits[threadIdx.x / 24][threadIdx.x % 24] = 0u;
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
             mbar_init(&stage_full[b], 1);
@@ -1238,12 +1279,218 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
+            if (nzmap)
+                inblock_round_bits(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, s_rowbits[b]);
+            else
+                inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
+        }
+        if (nzmap) {
+            // nonzero-row bits of this item (one column: CC = 1) in item-major
+            // order, nzmap[item * 24 + w]; k_bits_transpose reorders them for pass D
+            bar_compute(NCT);
+            if (warp == 0 && lane < 24) {
+                const int64_t it = blockIdx.x + i * gridDim.x;
+                nzmap[it * 24 + lane] = s_rowbits[b][lane];
+                s_rowbits[b][lane] = 0u;
+            }
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tile_done[b]);
     }
+}
+
+__global__ void k_popc_sum(const uint32_t *__restrict__ w, int64_t n, unsigned long long *out) {
+    unsigned long long acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += __popc(w[i]);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// Row bits of pass C, item-major (src[p * 24 + w], bit r of the 729-bit row
+// set of column p) -> row-major for pass D: bit q*PPR + p of dst (PPR = ppr
+// rounded up to 256). One CTA per 256 columns: the 256 x 24 source words in
+// smem, each thread builds output words (row q, 32 columns).
+__global__ void __launch_bounds__(256) k_bits_transpose(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
+                                                        int64_t ppr, int nrows, int64_t ppr_pad) {
+    __shared__ uint32_t sb[256 * 24];
+    const int64_t p0 = (int64_t)blockIdx.x * 256;
+    for (int t = threadIdx.x; t < 256 * 24; t += blockDim.x) {
+        const int64_t p = p0 + t / 24;
+        sb[t] = p < ppr ? src[p0 * 24 + t] : 0u;
+    }
+    __syncthreads();
+    const int64_t wpr = ppr_pad / 32;  // words per output row
+    for (int t = threadIdx.x; t < nrows * 8; t += blockDim.x) {
+        const int q = t >> 3, w = t & 7;  // row q, output word w of this CTA's 8
+        uint32_t o = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; i++) o |= ((sb[(32 * w + i) * 24 + (q >> 5)] >> (q & 31)) & 1u) << i;
+        dst[(int64_t)q * wpr + p0 / 32 + w] = o;
+    }
+}
+
+// Sparse reduce-only pass D over piece-major group 0. Pass C flagged the
+// nonzero 128-B rows of its output (k_bits_transpose puts the bits in D's
+// order); at n = 24 one row in four is nonzero. Only flagged rows are read
+// (cp.async) and written back (STG); the others are zero in memory already.
+// One CTA per SM, two tile buffers; every warp issues the loads of the next
+// item and the stores of the current one for the rows of its 32-row mask
+// word (warp k <-> rows 32k..32k+31), four rows per pass (8 lanes x 16 B).
+// Invariant: a buffer is zero outside the flagged rows of its last item
+// (zeroed at start; reduce keeps zero rows zero; the write-back zeroes them).
+template <int R1, int R2>
+__global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
+    k_reduce_sparse(uint32_t *__restrict__ state, const uint32_t *__restrict__ nzmap, int64_t nitems,
+                    uint32_t ib_mask, int64_t ncol, int64_t ppr_pad) {
+    using SM = PipeSmem<R1, R2>;
+    static_assert(pipe_cols<R1, R2>() == 1, "one 128-B column per tile");
+    constexpr int N1 = SM::N1, N2 = SM::N2, NR = SM::NR, CW = SM::CW, PITCH = SM::PITCH;
+    constexpr int NWB = (NR + 31) / 32;
+    static_assert(NWB <= CW, "one mask word per warp");
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ uint32_t msk[3][32];  // row masks of items i, i+1, i+2 (slot = item % 3)
+    __shared__ uint32_t rlist[32][16];  // per warp: the rows of its mask word (uint16)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 3, q16 = lane & 7;
+    constexpr int NCT = CW * 32;
+    const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto item = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+
+    // warp 0: the 729 row flags of item i as 23 mask words in msk[b]; the
+    // bitmap words of item i+1 are fetched now (their latency hides under an item)
+    uint32_t Wn = 0;
+    auto fetch = [&](int64_t i) {
+        if (warp == 0 && i < L) {
+            const int64_t it = item(i);
+            const int64_t B0 = (it / ncol) * ppr_pad + (it % ncol) * NR;
+            Wn = lane <= NWB ? __ldg(&nzmap[(B0 >> 5) + lane]) : 0u;
+        }
+    };
+    auto masks = [&](int64_t i) {
+        const int b = (int)(i % 3);
+        if (warp == 0) {
+            const int64_t it = item(i);
+            const int64_t B0 = (it / ncol) * ppr_pad + (it % ncol) * NR;
+            const int sh = (int)(B0 & 31);
+            const uint32_t W = Wn;
+            fetch(i + 1);
+            const uint32_t hi = __shfl_down_sync(0xffffffffu, W, 1);
+            uint32_t m = sh ? __funnelshift_r(W, hi, sh) : W;  // bits 32*lane .. 32*lane+31 of the span
+            const int r0 = 32 * lane;
+            if (r0 + 32 > NR) m &= r0 >= NR ? 0u : ((1u << (NR - r0)) - 1u);
+            if (lane < NWB) msk[b][lane] = m;
+        }
+    };
+    // warp k: cp.async of the flagged rows of mask word k of item i into buffer b
+    auto load = [&](int64_t i, int b) {
+        if (warp < NWB) {
+            const int64_t base = item(i) * NR;
+            uint32_t *tile = smem + b * SM::TILE_WORDS;
+            uint32_t mm = msk[i % 3][warp];
+            while (mm) {
+                uint32_t mg = mm;  // the g-th set bit of mm (g = 0..3)
+                if (g > 0) mg &= mg - 1;
+                if (g > 1) mg &= mg - 1;
+                if (g > 2) mg &= mg - 1;
+                const uint32_t j = (uint32_t)__ffs(mg) - 1u;
+                if (mg) {
+                    const int r = 32 * warp + (int)j;
+                    cp_async16(tile + r * PITCH + q16 * 4, state + (base + r) * 32 + q16 * 4, true);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++) mm &= mm - 1;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    for (int t = threadIdx.x; t < 2 * SM::TILE_WORDS / 4; t += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[t] = make_uint4(0, 0, 0, 0);
+    fetch(0);
+    if (L > 0) masks(0);
+    if (L > 1) masks(1);
+    __syncthreads();
+    if (L > 0) load(0, 0);
+    for (int64_t i = 0; i < L; i++) {
+        const int b = (int)(i & 1);
+        const int tb = b * SM::TILE_WORDS;
+        if (i + 2 < L) masks(i + 2);
+        __syncthreads();  // msk of i+2 visible; buffer b^1's previous write-back (zeroing) done
+        if (i + 1 < L) load(i + 1, b ^ 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's copies of item i
+        __syncthreads();                                       // everyone's
+        for (int t2 = warp; t2 < N2; t2 += CW) {
+            uint32_t v[N1];
+#pragma unroll
+            for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + lane];
+            if (!warp_any(v)) continue;
+            cube_reduce_par<R1>(v);
+#pragma unroll
+            for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + lane] = v[x];
+        }
+        if (R2 > 0) {
+            __syncthreads();
+            for (int t1 = warp; t1 < N1; t1 += CW) {
+                uint32_t v[N2];
+#pragma unroll
+                for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + lane];
+                if (!warp_any(v)) continue;
+                cube_reduce_par<R2>(v);
+#pragma unroll
+                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + lane] = v[x];
+            }
+        }
+        if (ib_mask) {
+            // in-block axes on the flagged rows only (the others are zero):
+            // warp k compacts the rows of mask word k, 8 rows x 4 blocks per pass
+            __syncthreads();
+            if (warp < NWB) {
+                const uint32_t mm = msk[i % 3][warp];
+                const int nrow = __popc(mm);
+                uint16_t *rl = reinterpret_cast<uint16_t *>(&rlist[warp][0]);
+                if ((mm >> lane) & 1u) rl[__popc(mm & ((1u << lane) - 1u))] = (uint16_t)(32 * warp + lane);
+                __syncwarp();
+                for (int e0 = 0; e0 < nrow; e0 += 8) {
+                    const int e = e0 + (lane >> 2);
+                    if (e < nrow) {
+                        uint4 *p = reinterpret_cast<uint4 *>(&smem[tb + rl[e] * PITCH + (lane & 3) * 8]);
+                        const uint4 x0 = p[0], x1 = p[1];
+                        uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                        inblock_reduce(v, ib_mask);
+                        p[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                        p[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // write back (and zero) the flagged rows of item i
+        if (warp < NWB) {
+            const int64_t base = item(i) * NR;
+            uint32_t *tile = smem + tb;
+            uint32_t mm = msk[i % 3][warp];
+            while (mm) {
+                uint32_t mg = mm;  // the g-th set bit of mm (g = 0..3)
+                if (g > 0) mg &= mg - 1;
+                if (g > 1) mg &= mg - 1;
+                if (g > 2) mg &= mg - 1;
+                const uint32_t j = (uint32_t)__ffs(mg) - 1u;
+                if (mg) {
+                    const int r = 32 * warp + (int)j;
+                    uint4 *sp = reinterpret_cast<uint4 *>(tile + r * PITCH) + q16;
+                    const uint4 x = *sp;
+                    *sp = make_uint4(0, 0, 0, 0);
+                    reinterpret_cast<uint4 *>(state + (base + r) * 32)[q16] = x;
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++) mm &= mm - 1;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1367,6 +1614,8 @@ struct Engine {
     cudaStream_t stream = nullptr;
     uint32_t *state = nullptr;
     size_t state_cap = 0;  // bytes
+    uint32_t *nzmap = nullptr;  // nonzero-piece bitmap of pass C (sparse pass D)
+    size_t nzmap_cap = 0;       // bytes
     int64_t *tile_base = nullptr, *tile_pos = nullptr;
     int32_t *tile_cnt = nullptr;
     size_t tile_cap = 0, tile_pos_cap = 0, tile_cnt_cap = 0;  // entries
@@ -1508,6 +1757,10 @@ int ensure_attrs() {
     int rc;
     if ((rc = set_mode_attrs<MERGE_ONLY>())) return rc;  // pass B (k_strided)
     if ((rc = set_pipe_attrs<REDUCE_ONLY>())) return rc;  // pass D (k_strided_pipe)
+    {
+        using SMD = PipeSmem<3, 3>;
+        CK(cudaFuncSetAttribute(k_reduce_sparse<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMD::SMEM));
+    }
     if ((rc = set_mr_attr<1, 0>()) || (rc = set_mr_attr<2, 0>()) || (rc = set_mr_attr<3, 0>()) ||
         (rc = set_mr_attr<2, 2>()) || (rc = set_mr_attr<3, 2>()) || (rc = set_mr_attr<3, 3>()))
         return rc;
@@ -1652,7 +1905,8 @@ int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2
 }
 
 template <int R1, int R2, int MODE>
-int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s) {
+int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s,
+                uint32_t *nzmap) {
     using SM = PipeSmem<R1, R2>;
     constexpr int CC = pipe_cols<R1, R2>();  // 128-B columns per tile
     CUtensorMap map, gmap;
@@ -1672,7 +1926,8 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     const int64_t nitems = ncolg * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
-        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, g_sparse);
+        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, g_sparse,
+                                                                          nzmap);
     else
         k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, pm ? 1 : 0,
                                                                           g_sparse);
@@ -1682,14 +1937,14 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
 
 template <int MODE>
 int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s,
-                     bool pm = false) {
+                     bool pm = false, uint32_t *nzmap = nullptr) {
     switch (r) {
-        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
+        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
+        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
+        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
+        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
+        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s, nzmap);
     }
 }
 
@@ -1882,13 +2137,35 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
 int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s) {
     const uint64_t S = (uint64_t)p.nblocks * 32;
     int rc;
+    // sparse pass D (k_reduce_sparse): piece-major group 0 behind a fused C
+    // with two groups; C flags its nonzero pieces
+    // Opt-in (DQMC_SPARSE_D=1): measured slower than the dense TMA pass at n = 24
+    // (D 11.7 vs 11.6 ms, C +1.1 ms for the bits): with two 93 KB tile buffers
+    // per SM too few flagged rows are in flight.
+    const bool sparse_d = fused && p.pm && p.m == 2 && p.r[0] == 6 && p.r[1] == 6 && p.ib_C && getenv("DQMC_SPARSE_D");
+    // row bits: item-major from C (ppr x 24 words), then row-major for D
+    // (729 rows x PPR bits, PPR = ppr rounded up to 256, + one word of slack)
+    const int64_t ppr = sparse_d ? pow3l(p.a[1] - p.g) * p.pitch / kRowBlocks : 0;
+    const int64_t ppr_pad = (ppr + 255) / 256 * 256;
+    uint32_t *bits_c = nullptr, *bits_d = nullptr;
+    if (sparse_d) {
+        const size_t wc = (size_t)ppr * 24, wd = (size_t)729 * (ppr_pad / 32) + 64;
+        if ((rc = grow(g_eng.nzmap, g_eng.nzmap_cap, (wc + wd) * 4, 1))) return rc;
+        bits_c = g_eng.nzmap;
+        bits_d = g_eng.nzmap + wc;
+    }
     {
         const int k = p.m - 1;
         const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         if (fused) {
-            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
+            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s, false, bits_c))) return rc;
             tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(S * std::pow(2.0 / 3.0, p.r[k]) + S));
+            if (sparse_d) {
+                k_bits_transpose<<<(unsigned)((ppr + 255) / 256), 256, 0, s>>>(bits_c, bits_d, ppr, 729, ppr_pad);
+                CK(cudaGetLastError());
+                tm.mark("k_bits_transpose", (uint64_t)ppr * 24 * 4 * 2);
+            }
         } else {
             if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
             tm.mark("k_strided<REDUCE>", 2 * S);
@@ -1899,6 +2176,25 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
+        if (k == 0 && sparse_d) {
+            using SMD = PipeSmem<3, 3>;
+            const int64_t nitems = (Q / kRowBlocks) * pow3l(above);
+            const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
+            k_reduce_sparse<3, 3><<<grid, SMD::CW * 32, SMD::SMEM, s>>>(state, bits_d, nitems, p.ib_D[k],
+                                                                        Q / kRowBlocks, ppr_pad);
+            CK(cudaGetLastError());
+            tm.mark("k_reduce_sparse", 2 * S);
+            if (tm.on && !tm.bytes.empty()) {  // timing mode: the bytes it moved, 2 x 128 B per flagged piece
+                const int64_t nw = (int64_t)729 * (ppr_pad / 32);
+                CK(cudaMemsetAsync(g_eng.alloc + 2, 0, 8, s));
+                k_popc_sum<<<(unsigned)std::min<int64_t>((nw + 255) / 256, 4096), 256, 0, s>>>(bits_d, nw, g_eng.alloc + 2);
+                unsigned long long nz = 0;
+                CK(cudaMemcpyAsync(&nz, g_eng.alloc + 2, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                tm.bytes.back() = 2ull * 128 * nz;
+            }
+            continue;
+        }
         if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above), p.ib_D[k], s, k == 0 && p.pm)))
             return rc;
         tm.mark("k_strided<REDUCE>", 2 * S);

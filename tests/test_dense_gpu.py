@@ -199,6 +199,21 @@ class TestFullSize:
         hr = pkg.prime_ranks_from_values(v.cpu().numpy())
         assert np.array_equal(hr, host)
 
+    def test_config4_n24_plan_variants(self, pkg, golden, monkeypatch):
+        """The opt-in plan variants (sparse pass D over C's nonzero-row bits;
+        the contiguous-tile layout without piece-major group 0) give the same
+        ranks as the default plan."""
+        from paper_2302_10083_b200 import device
+
+        g = golden["configs"]["4"]
+        v = device.gen3_device(24, 0.75, 0.05, 3)
+        for env in ("DQMC_SPARSE_D", "DQMC_NO_PM"):
+            monkeypatch.setenv(env, "1")
+            r, cnt = device.dense_prime_ranks_device(v, 24)
+            monkeypatch.delenv(env)
+            assert cnt == g["primes"], env
+            assert rsha(r.cpu().numpy())[:16] == g["ranks_sha256_prefix"], env
+
 
 @pytest.mark.slow
 class TestLargestSingleGpu:
