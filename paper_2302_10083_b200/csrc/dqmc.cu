@@ -1493,6 +1493,129 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Block-sparse pass D (piece-major group 0, 3^6 rows, one column): the tile's
+// 729 rows are 27 sub-blocks of 27 consecutive rows (one value of the three
+// high group-0 digits). Pass C's row bits (k_bits_transpose order) say which
+// sub-blocks hold a nonzero row: at n = 24 about half of them
+// (tools/sparsity.py). Only those are loaded and stored, each as one TMA box
+// of 27 rows x 128 B; the compute warps zero-fill the others in shared memory.
+template <int R1, int R2>
+__global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
+    k_reduce_blocks(const __grid_constant__ CUtensorMap smap, const uint32_t *__restrict__ nzmap, int64_t ncol,
+                    int64_t nitems, uint32_t ib_mask, int64_t ppr_pad) {
+    using SM = PipeSmem<R1, R2>;
+    static_assert(pipe_cols<R1, R2>() == 1 && SM::NR == 729, "3^6 rows, one column");
+    constexpr int N1 = SM::N1, N2 = SM::N2, NR = SM::NR, CW = SM::CW, PITCH = SM::PITCH;
+    constexpr int SB = 27, NSB = NR / SB, SBW = SB * PITCH;  // sub-block rows, count, words
+    constexpr int NWB = (NR + 31) / 32;
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ __align__(8) uint64_t full[2], computed[2];
+    __shared__ uint32_t s_F[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto item = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&full[b], 1);
+            mbar_init(&computed[b], CW);
+        }
+    }
+    __syncthreads();
+
+    if (warp == CW) {  // ------------------------------ producer warp
+        uint32_t Fb[2] = {0u, 0u};
+        for (int64_t i = 0; i < L + 2; i++) {
+            const int b = (int)(i & 1);
+            uint32_t *tile = smem + b * SM::TILE_WORDS;
+            if (i >= 2) {  // store the loaded sub-blocks of item i-2
+                mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
+                const int64_t it = item(i - 2);
+                if (lane == 0) {
+                    uint32_t F = Fb[b];
+                    while (F) {
+                        const int k = __ffs(F) - 1;
+                        F &= F - 1;
+                        tma_store_4d(&smap, 0, SB * k, (int)(it % ncol), (int)(it / ncol), tile + k * SBW);
+                    }
+                    bulk_commit();
+                    bulk_wait_read<0>();  // buffer b is reloaded next
+                }
+                __syncwarp();
+            }
+            if (i < L) {
+                const int64_t it = item(i);
+                // sub-block flags from the 729 row bits (lane k < 27: rows 27k..27k+26)
+                const int64_t B0 = (it / ncol) * ppr_pad + (it % ncol) * NR;
+                const int sh = (int)(B0 & 31);
+                const uint32_t W = lane <= NWB ? __ldg(&nzmap[(B0 >> 5) + lane]) : 0u;
+                const int q = sh + SB * (lane < NSB ? lane : 0);
+                const uint32_t w0 = __shfl_sync(0xffffffffu, W, (q >> 5) & 31);
+                const uint32_t w1 = __shfl_sync(0xffffffffu, W, ((q >> 5) + 1) & 31);
+                const uint32_t bits = __funnelshift_r(w0, w1, q & 31) & ((1u << SB) - 1u);
+                const uint32_t F = __ballot_sync(0xffffffffu, lane < NSB && bits != 0u);
+                Fb[b] = F;
+                if (lane == 0) {
+                    s_F[b] = F;
+                    mbar_expect_tx(&full[b], (unsigned)(__popc(F) * SB * 128));
+                    uint32_t G = F;
+                    while (G) {
+                        const int k = __ffs(G) - 1;
+                        G &= G - 1;
+                        tma_load_4d(tile + k * SBW, &smap, 0, SB * k, (int)(it % ncol), (int)(it / ncol), &full[b]);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (lane == 0) bulk_wait0();
+        return;
+    }
+
+    // ---------------------------------- compute warps
+    constexpr int NCT = CW * 32;
+    for (int64_t i = 0; i < L; i++) {
+        const int b = (int)(i & 1);
+        const int tb = b * SM::TILE_WORDS;
+        mbar_wait(&full[b], (unsigned)((i >> 1) & 1));
+        const uint32_t F = s_F[b];
+        if (F) {
+            if (F != (1u << NSB) - 1u) {  // zero the sub-blocks that were not loaded
+                for (int t = threadIdx.x; t < NSB * (SBW / 4); t += NCT) {
+                    const int k = t / (SBW / 4);
+                    if (!((F >> k) & 1u)) reinterpret_cast<uint4 *>(smem + tb)[t] = make_uint4(0, 0, 0, 0);
+                }
+                bar_compute(NCT);
+            }
+            for (int t2 = warp; t2 < N2; t2 += CW) {
+                uint32_t v[N1];
+#pragma unroll
+                for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + lane];
+                if (!warp_any(v)) continue;
+                cube_reduce_par<R1>(v);
+#pragma unroll
+                for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + lane] = v[x];
+            }
+            bar_compute(NCT);
+            for (int t1 = warp; t1 < N1; t1 += CW) {
+                uint32_t v[N2];
+#pragma unroll
+                for (int x = 0; x < N2; x++) v[x] = smem[tb + (t1 + N1 * x) * PITCH + lane];
+                if (!warp_any(v)) continue;
+                cube_reduce_par<R2>(v);
+#pragma unroll
+                for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + lane] = v[x];
+            }
+            if (ib_mask) {  // zero sub-blocks are skipped warp by warp
+                bar_compute(NCT);
+                inblock_round(&smem[tb], NR * kRowBlocks, ib_mask, NCT, 1);
+            }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&computed[b]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -1760,6 +1883,7 @@ int ensure_attrs() {
     {
         using SMD = PipeSmem<3, 3>;
         CK(cudaFuncSetAttribute(k_reduce_sparse<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMD::SMEM));
+        CK(cudaFuncSetAttribute(k_reduce_blocks<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMD::SMEM));
     }
     if ((rc = set_mr_attr<1, 0>()) || (rc = set_mr_attr<2, 0>()) || (rc = set_mr_attr<3, 0>()) ||
         (rc = set_mr_attr<2, 2>()) || (rc = set_mr_attr<3, 2>()) || (rc = set_mr_attr<3, 3>()))
@@ -2139,10 +2263,13 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
     int rc;
     // sparse pass D (k_reduce_sparse): piece-major group 0 behind a fused C
     // with two groups; C flags its nonzero pieces
-    // Opt-in (DQMC_SPARSE_D=1): measured slower than the dense TMA pass at n = 24
-    // (D 11.7 vs 11.6 ms, C +1.1 ms for the bits): with two 93 KB tile buffers
-    // per SM too few flagged rows are in flight.
-    const bool sparse_d = fused && p.pm && p.m == 2 && p.r[0] == 6 && p.r[1] == 6 && p.ib_C && getenv("DQMC_SPARSE_D");
+    // Opt-in experiments, both bit-exact and both no faster than the dense TMA
+    // pass at n = 24: DQMC_SPARSE_D=1 k_reduce_sparse (flagged
+    // rows, cp.async), 2 k_reduce_blocks (27-row sub-blocks holding a flagged
+    // row, TMA boxes). C then records its nonzero rows (+1.1 ms).
+    const char *sd_env = getenv("DQMC_SPARSE_D");
+    const int sparse_mode = sd_env ? atoi(sd_env) : 0;
+    const bool sparse_d = fused && p.pm && p.m == 2 && p.r[0] == 6 && p.r[1] == 6 && p.ib_C && sparse_mode > 0;
     // row bits: item-major from C (ppr x 24 words), then row-major for D
     // (729 rows x PPR bits, PPR = ppr rounded up to 256, + one word of slack)
     const int64_t ppr = sparse_d ? pow3l(p.a[1] - p.g) * p.pitch / kRowBlocks : 0;
@@ -2180,8 +2307,15 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
             using SMD = PipeSmem<3, 3>;
             const int64_t nitems = (Q / kRowBlocks) * pow3l(above);
             const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
-            k_reduce_sparse<3, 3><<<grid, SMD::CW * 32, SMD::SMEM, s>>>(state, bits_d, nitems, p.ib_D[k],
-                                                                        Q / kRowBlocks, ppr_pad);
+            if (sparse_mode == 2) {
+                CUtensorMap smap;
+                if ((rc = make_group_map4(&smap, state, Q, 729, pow3l(above), 27, 32, true))) return rc;
+                k_reduce_blocks<3, 3><<<grid, SMD::THREADS, SMD::SMEM, s>>>(smap, bits_d, Q / kRowBlocks, nitems,
+                                                                            p.ib_D[k], ppr_pad);
+            } else {
+                k_reduce_sparse<3, 3><<<grid, SMD::CW * 32, SMD::SMEM, s>>>(state, bits_d, nitems, p.ib_D[k],
+                                                                            Q / kRowBlocks, ppr_pad);
+            }
             CK(cudaGetLastError());
             tm.mark("k_reduce_sparse", 2 * S);
             if (tm.on && !tm.bytes.empty()) {  // timing mode: the bytes it moved, 2 x 128 B per flagged piece

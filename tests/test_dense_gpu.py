@@ -207,8 +207,8 @@ class TestFullSize:
 
         g = golden["configs"]["4"]
         v = device.gen3_device(24, 0.75, 0.05, 3)
-        for env in ("DQMC_SPARSE_D", "DQMC_NO_PM"):
-            monkeypatch.setenv(env, "1")
+        for env, val in (("DQMC_SPARSE_D", "1"), ("DQMC_SPARSE_D", "2"), ("DQMC_NO_PM", "1")):
+            monkeypatch.setenv(env, val)
             r, cnt = device.dense_prime_ranks_device(v, 24)
             monkeypatch.delenv(env)
             assert cnt == g["primes"], env

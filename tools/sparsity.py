@@ -37,5 +37,8 @@ if T >= 6:
     print(f"D tiles (q2, x over q1) nonzero: {pc.any(1).float().mean().item():.4f}")
     # C's tiles: (q1, x) over the upper digits
     print(f"C tiles (q1, x over upper) nonzero: {pc.any(0).float().mean().item():.4f}")
-    # per-digit-star structure: nonzero pieces by star count of the upper digits
+    # D-tile sub-blocks of g consecutive group-0 rows (the low log3(g) digits vary)
+    for gsz in (3, 9, 27, 81, 243):
+        sb = pc.permute(0, 2, 1).reshape(3**(T - r0), -1, 729 // gsz, gsz).any(3)
+        print(f"D sub-blocks of {gsz} rows nonzero: {sb.float().mean().item():.4f}")
 del M
