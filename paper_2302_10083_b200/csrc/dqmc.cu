@@ -1262,13 +1262,15 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
 #pragma unroll
                 for (int x = 0; x < N2; x++) smem[tb + (t1 + N1 * x) * PITCH + 32 * h + lane] = v[x];
             }
+        }
+        if (R2 > 0) {
             bar_compute(NCT);
             for (int tt = warp; tt < N2 * CC; tt += CW) {
                 const int t2 = tt % N2, h = tt / N2;
                 uint32_t v[N1];
 #pragma unroll
                 for (int x = 0; x < N1; x++) v[x] = smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane];
-                if (sparse && !warp_any(v)) continue;
+                if ((sparse & 1) && !warp_any(v)) continue;
                 cube_reduce_par<R1>(v);
 #pragma unroll
                 for (int x = 0; x < N1; x++) smem[tb + (x + N1 * t2) * PITCH + 32 * h + lane] = v[x];
@@ -1282,7 +1284,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             if (nzmap)
                 inblock_round_bits(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, s_rowbits[b]);
             else
-                inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
+                inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse & 1);
         }
         if (nzmap) {
             // nonzero-row bits of this item (one column: CC = 1) in item-major
@@ -2050,8 +2052,8 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     const int64_t nitems = ncolg * nouter;
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
-        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, g_sparse,
-                                                                          nzmap);
+        k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(
+            map, gmap, ncolg, nitems, ib, g_sparse, nzmap);
     else
         k_strided_pipe<R1, R2, MODE><<<grid, SM::THREADS, SM::SMEM, s>>>(map, gmap, ncolg, nitems, ib, pm ? 1 : 0,
                                                                           g_sparse);
@@ -3108,6 +3110,7 @@ void dqmc_release(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_eng.device < 0) return;
     cudaFree(g_eng.state);
+    cudaFree(g_eng.nzmap);
     cudaFree(g_eng.tile_base);
     cudaFree(g_eng.tile_pos);
     cudaFree(g_eng.tile_cnt);
