@@ -12,8 +12,9 @@ inputs from the reference's frozen generator.
          passes, compaction of all prime ranks into an HBM int64 buffer).
   e2e    the public host API with a pinned host input and the int64 rank array
          returned on the host: H2D of the table and D2H of every rank inside
-         each timed step. Headline: K calls through stream_prime_ranks (two in
-         flight, call i's D2H overlapping call i+1's passes); single_call: one
+         each timed step. Headline: a batch of max(K, 30) calls through
+         stream_prime_ranks (three in flight, call i's D2H overlapping call
+         i+1's passes; the batch fills and drains once); single_call: one
          synchronous prime_ranks_from_values call.
   roofline  the dominant kernel's algorithmic bytes per launch / its
          CUDA-event duration vs MEASURED_PEAKS.json hbm_gbs.
@@ -41,6 +42,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 WORKLOAD = dict(n=24, p_on=0.75, p_dc=0.05, seed=3)  # BASELINE config 4
+E2E_MIN_CALLS = 30  # calls per timed job-stream batch (fill + drain amortised)
 METRIC = "ternary cells/s to all prime implicants"
 UNIT = "cells/s"
 
@@ -280,15 +282,18 @@ def run_engine_bench(args):
         del res
     t_single = sum(e2e_times) / len(e2e_times)
     # the headline e2e: K calls through the job stream (dqmc_submit_u8 /
-    # dqmc_collect, two in flight). Every step still copies its table from pinned
+    # dqmc_collect, three in flight). Every step still copies its table from pinned
     # host memory and its full rank array back to the host inside the timed
     # region; call i's D2H overlaps call i+1's passes.
-    for r in pkg.stream_prime_ranks([hv] * 2):  # warm the job slots for this n
+    # The stream fills (the first call's passes) and drains (the last call's
+    # D2H) once per batch, so the batch is at least E2E_MIN_CALLS calls long.
+    for r in pkg.stream_prime_ranks([hv] * 3):  # warm the job slots for this n
         del r
+    n_stream = max(args.steps, E2E_MIN_CALLS)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     got = 0
-    for r in pkg.stream_prime_ranks([hv] * args.steps):
+    for r in pkg.stream_prime_ranks([hv] * n_stream):
         assert len(r) == cnt
         got += 1
         del r
@@ -336,7 +341,8 @@ def run_engine_bench(args):
             "h2d_bytes_per_step": int(1 << n),
             "d2h_bytes_per_step": int(cnt * 8 + 8),
             "api": "paper_2302_10083_b200.stream_prime_ranks (C ABI dqmc_submit_u8 / dqmc_collect), "
-                   "two calls in flight, pinned input",
+                   "three calls in flight, pinned input",
+            "calls": n_stream,
             "single_call": {
                 "value": 3**n / t_single,
                 "ms": t_single * 1e3,

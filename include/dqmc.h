@@ -91,7 +91,7 @@ int dqmc_primes_u8(const uint8_t *values, int n, int h, uint64_t mem_cap, uint32
                    dqmc_result_t *out);
 void dqmc_free_result(dqmc_result_t *res);
 
-/* The same calls as a stream of jobs (at most two outstanding, collected in
+/* The same calls as a stream of jobs (at most three outstanding, collected in
  * submission order). dqmc_submit_* queues the table's H2D, every pass and the
  * final stage, and returns; dqmc_collect waits for that job and copies its
  * ranks to the host while the device already runs the next job, so call i's

@@ -117,7 +117,7 @@ def prime_ranks_from_values(
 
 class PrimeJob:
     """A submitted call (dqmc_submit_*): ``result()`` waits for it and returns
-    the int64 ranks. Keeps its input alive until collected. At most two jobs
+    the int64 ranks. Keeps its input alive until collected. At most three jobs
     may be outstanding; they are collected in submission order."""
 
     def __init__(self, job_id: int, keep):
@@ -152,12 +152,13 @@ def submit(table) -> PrimeJob:
 
 
 def stream_prime_ranks(tables):
-    """Prime ranks of every table of an iterable, in order, with two calls in
-    flight: call i's device-to-host copy overlaps call i+1's passes."""
+    """Prime ranks of every table of an iterable, in order, with three calls in
+    flight: call i's device-to-host copy overlaps call i+1's passes while call
+    i+2 is already queued behind them (dqmc_submit_* / dqmc_collect)."""
     pending = []
     for t in tables:
         pending.append(submit(t))
-        if len(pending) == 2:
+        if len(pending) == 3:
             yield pending.pop(0).result()
     while pending:
         yield pending.pop(0).result()

@@ -311,7 +311,7 @@ class TestAsyncAndGraph:
 
 
 class TestJobStream:
-    """dqmc_submit_* / dqmc_collect: two calls in flight, results identical to
+    """dqmc_submit_* / dqmc_collect: three calls in flight, results identical to
     the synchronous call, edge cases of the job protocol."""
 
     def test_stream_matches_sync(self, pkg, gen_mod):
@@ -340,10 +340,10 @@ class TestJobStream:
 
     def test_protocol_errors(self, pkg, gen_mod):
         t = gen_mod.gen3(12, 0.5, 0.0, 1)
-        a, b = pkg.submit(t), pkg.submit(t)
+        a, b, c = pkg.submit(t), pkg.submit(t), pkg.submit(t)
         with pytest.raises(ValueError):
-            pkg.submit(t)  # a third outstanding job
+            pkg.submit(t)  # a fourth outstanding job
         with pytest.raises(ValueError):
             b.result()  # out of order
-        ra, rb = a.result(), b.result()
-        assert np.array_equal(ra, rb) and np.array_equal(ra, pkg.prime_ranks_from_values(t))
+        ra, rb, rc = a.result(), b.result(), c.result()
+        assert np.array_equal(ra, rb) and np.array_equal(ra, rc) and np.array_equal(ra, pkg.prime_ranks_from_values(t))
