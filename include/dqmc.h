@@ -41,8 +41,12 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+/* the library is built with -fvisibility=hidden: only these symbols export */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 
-#define DQMC_ABI_VERSION 1
+#define DQMC_ABI_VERSION 2
 
 /* status codes */
 #define DQMC_OK 0
@@ -173,26 +177,30 @@ int dqmc_gen3_host(uint8_t *values_host, int n, double p_on, double p_dc, uint64
 int dqmc_gen_sbox_host(uint8_t *values_host, uint64_t seed); /* 2^20 bytes */
 int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_t *out_host);
 
-/* Building blocks of the sharded multi-GPU path, all on
- * device buffers in the h = 5 layout (n >= 5):
+/* Building blocks of the sharded multi-GPU path (SURVEY.md §8(e),
+ * DESIGN.md §6), all on device buffers in the h = 5 layout (n >= 5):
  * dqmc_merge_device: complete MERGE of all n dimensions (no REDUCE) into
  *   state_out (dqmc_state_bytes(n, 5) bytes) — the implicant bitmap M of
  *   the (sub-)function, DenseState.words after run_pass(MERGE) (dense.py:296-315).
  * dqmc_reduce_extract_device: REDUCE of all n dimensions in place, then clear
- *   the cells set in kill (may be NULL; the OR of the top-axis parent bitmaps),
- *   then ordered compaction of the survivors as ranks + rank_offset.
+ *   every cell set in any of the nkill (<= 8) bitmaps kills[] — the top-axis
+ *   parent super-blocks, pre-reduce, read in place (local or peer memory) —
+ *   then ordered compaction of the survivors as ranks + rank_offset. ranks_dev
+ *   NULL or DQMC_FLAG_COUNT_ONLY: count only. If the count exceeds ranks_cap,
+ *   *count_out is the true count and nothing beyond ranks_cap is written.
  * dqmc_bitop_device: dst = a & b (op 0) or a | b (op 1), nbytes % 16 == 0. */
 int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state_out, void *stream);
-int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *kill, int64_t rank_offset, int64_t *ranks_dev,
-                               int64_t ranks_cap, int64_t *count_out, uint32_t flags, void *stream);
+int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *const *kills, int nkill, int64_t rank_offset,
+                               int64_t *ranks_dev, int64_t ranks_cap, int64_t *count_out, uint32_t flags,
+                               void *stream);
 int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint64_t nbytes, int op, void *stream);
 
 /* Peer access for the sharded path's P2P transport (one process per GPU):
- * a rank exports a CUDA IPC handle of the allocation holding one of its
- * blocks, plus the block's byte offset inside it; a peer opens the handle
- * (once per allocation) and passes base + offset straight to
- * dqmc_bitop_device, so the AND / OR kernels read the peer's memory over
- * NVLink with no staging copy. handle is 64 bytes
+ * a rank exports a CUDA IPC handle of the allocation holding its arena of
+ * super-blocks, plus the arena's byte offset inside it; a peer opens the
+ * handle once and passes base + offset + slot straight to dqmc_bitop_device
+ * and dqmc_reduce_extract_device, so the AND kernel and the final pass read
+ * the peer's memory over NVLink with no staging copy. handle is 64 bytes
  * (cudaIpcMemHandle_t). dqmc_ipc_open also enables peer access between the
  * current device and the allocation's device when they differ. */
 int dqmc_ipc_get(const void *dev_ptr, void *handle_out, uint64_t *offset_out);
@@ -204,9 +212,24 @@ int dqmc_ipc_close(void *base);
  * (32 int64 entries). Returns the number written. */
 int dqmc_plan(int n, int64_t *out, int max);
 
-/* Release all cached device/host workspaces. */
+/* Release all cached device/host workspaces (waits for the device first). */
 void dqmc_release(void);
 
+/* Ordering and lifetime of the engine workspace for callers that replay
+ * captured CUDA graphs of DQMC_FLAG_ASYNC calls. Every entry point orders its
+ * own work after every earlier use of the shared workspace (one event), but a
+ * graph replay is the caller's launch: bracket it with dqmc_engine_enter
+ * (stream waits for earlier engine work) and dqmc_engine_exit (later calls
+ * wait for the replay). dqmc_engine_generation changes whenever a workspace
+ * buffer is reallocated or released; a graph captured under another
+ * generation holds dangling pointers and must not be replayed. */
+uint64_t dqmc_engine_generation(void);
+int dqmc_engine_enter(void *stream);
+int dqmc_engine_exit(void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

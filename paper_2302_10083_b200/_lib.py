@@ -66,6 +66,9 @@ EXPORTS = (
     "dqmc_bitop_device",
     "dqmc_plan",
     "dqmc_release",
+    "dqmc_engine_generation",
+    "dqmc_engine_enter",
+    "dqmc_engine_exit",
     "dqmc_state_create",
     "dqmc_state_free",
     "dqmc_state_info",
@@ -156,10 +159,14 @@ def load() -> ctypes.CDLL:
             "dqmc_ipc_close": (i32, [vp]),
             "dqmc_order_by_weight": (i32, [vp, i64, i32, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
-            "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),
+            "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i32, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32,
+                                                 vp]),
             "dqmc_bitop_device": (i32, [vp, vp, vp, u64, i32, vp]),
             "dqmc_plan": (i32, [i32, ctypes.POINTER(ctypes.c_int64), i32]),
             "dqmc_release": (None, []),
+            "dqmc_engine_generation": (u64, []),
+            "dqmc_engine_enter": (i32, [vp]),
+            "dqmc_engine_exit": (i32, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -1,0 +1,682 @@
+// dqmc_final.cu — final stage E: REDUCE of the C0 axes, popcount and ordered
+// compaction (extract_ranks, dense.py:376-397).
+//
+// Rank order is memory order in the reference layout (block a, bit b = rank
+// a*243 + b), so compaction needs no sort: each tile reserves a range of a
+// scratch buffer with one atomic, a scan of the per-tile counts gives every
+// tile its rank-order position, and k_reorder moves the ranks there.
+#include <cub/device/device_scan.cuh>
+
+#include "dqmc_internal.cuh"
+
+namespace dqmc {
+namespace {
+
+// REDUCE along C0 axes [j0, j0+K) with register sub-cubes, lane = word.
+template <int K>
+__device__ void tile_reduce_axes(uint32_t *sm, int g, int j0) {
+    constexpr int N = P3<K>::v;
+    const int sj = (int)pow3l(j0);
+    const int span = sj * N;
+    const int nhi = (int)pow3l(g) / span;
+    const int ntask = sj * nhi * 8;
+    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+        const int w = t & 7, q = t >> 3;
+        const int lo = q % sj, hi = q / sj;
+        const int blk = lo + hi * span;
+        uint32_t v[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) v[i] = sm[(blk + i * sj) * 8 + w];
+        cube_reduce_par<K>(v);
+#pragma unroll
+        for (int i = 0; i < N; i++) sm[(blk + i * sj) * 8 + w] = v[i];
+    }
+    __syncthreads();
+}
+
+__device__ void tile_reduce_c0(uint32_t *sm, int g) {
+    int j = 0;
+    while (g - j >= 3) {
+        tile_reduce_axes<3>(sm, g, j);
+        j += 3;
+    }
+    if (g - j == 2) tile_reduce_axes<2>(sm, g, j);
+    if (g - j == 1) tile_reduce_axes<1>(sm, g, j);
+}
+
+
+// In-block reduce, popcount and ordered compaction of one tile
+// (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order is
+// rank order, so the output needs no sort). Warp w owns the contiguous block
+// range [b0, b1); lane l takes blocks b0+l, b0+l+32, ... (group j = the j-th
+// 32 blocks). Block counts stay in registers, two 16-bit fields per word, so
+// one packed warp scan serves every group: the phases are short latency
+// chains, which is what bounds this pass (3 CTAs/SM, smem-limited).
+template <int NT>
+__device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
+    constexpr int kMaxIter = ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;  // ceil(max warp range / 32)
+    constexpr int kPk = (kMaxIter + 1) / 2;
+    __shared__ int64_t s_warp_off[NT / 32];
+    __shared__ int64_t s_tile_off;
+    __shared__ uint16_t s_cnt[NT / 32][kMaxIter][32];  // slow-path block popcounts, then the emission list
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
+    const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
+
+    // (1) lane = block: popcount (+ in-block axes, kills, bitmap on the slow path)
+    uint32_t pk[kPk];
+#pragma unroll
+    for (int i = 0; i < kPk; i++) pk[i] = 0;
+    if (!fa.ib_mask && !fa.nkill && !fa.bitmap_out) {  // count only: word order does not matter
+#pragma unroll
+        for (int j = 0; j < kMaxIter; j++) {
+            const int b = b0 + 32 * j + lane;
+            if (b < b1) {
+                const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+                const uint4 x0 = p[h], x1 = p[h ^ 1];
+                const uint32_t cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) +
+                                    __popc(x1.y) + __popc(x1.z) + __popc(x1.w);
+                pk[j >> 1] |= cj << (16 * (j & 1));
+            }
+        }
+    } else {
+        // rolled (the in-block code is large: the kernel must stay inside the instruction cache)
+#pragma unroll 1
+        for (int j = 0; j < kMaxIter; j++) {
+            const int b = b0 + 32 * j + lane;
+            int cj = 0;
+            if (b < b1) {
+                uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
+                const uint4 ya = p[h], yb = p[h ^ 1];
+                uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
+                if (fa.ib_mask) {
+                    uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    inblock_reduce(v, fa.ib_mask);
+                    x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                    x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                }
+                if (fa.nkill) {
+                    // top-axis parents (sharded path): OR of up to kMaxKill
+                    // bitmaps read in place, local or peer memory over NVLink
+                    uint4 k0 = make_uint4(0, 0, 0, 0), k1 = k0;
+#pragma unroll 1
+                    for (int q = 0; q < fa.nkill; q++) {
+                        const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill[q] + (blk0 + b) * 8);
+                        const uint4 a0 = kq[0], a1 = kq[1];
+                        k0 = make_uint4(k0.x | a0.x, k0.y | a0.y, k0.z | a0.z, k0.w | a0.w);
+                        k1 = make_uint4(k1.x | a1.x, k1.y | a1.y, k1.z | a1.z, k1.w | a1.w);
+                    }
+                    x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
+                    x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
+                }
+                if (fa.ib_mask || fa.nkill) {
+                    p[h] = h ? x1 : x0;
+                    p[h ^ 1] = h ? x0 : x1;
+                }
+                if (fa.bitmap_out) {
+                    uint4 *q = reinterpret_cast<uint4 *>(fa.bitmap_out + (blk0 + b) * 8);
+                    q[0] = x0;
+                    q[1] = x1;
+                }
+                cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
+                     __popc(x1.z) + __popc(x1.w);
+            }
+            s_cnt[warp][j][lane] = (uint16_t)cj;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kMaxIter; j++) pk[j >> 1] |= (uint32_t)s_cnt[warp][j][lane] << (16 * (j & 1));
+    }
+
+    // (2) packed inclusive warp scan (fields <= 32 * 243 < 2^16: no carries
+    //     between fields), group bases, the warp's total
+    uint32_t inc[kPk];
+#pragma unroll
+    for (int i = 0; i < kPk; i++) inc[i] = pk[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < kPk; i++) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc[i], o);
+            if (lane >= o) inc[i] += y;
+        }
+    }
+    int gbase[kMaxIter];
+    int wsum = 0;
+#pragma unroll
+    for (int i = 0; i < kPk; i++) {
+        const uint32_t t = __shfl_sync(0xffffffffu, inc[i], 31);
+        gbase[2 * i] = wsum;
+        wsum += (int)(t & 0xffffu);
+        if (2 * i + 1 < kMaxIter) {
+            gbase[2 * i + 1] = wsum;
+            wsum += (int)(t >> 16);
+        }
+    }
+    if (lane == 0) s_warp_off[warp] = wsum;
+    __syncthreads();
+
+    // (3) reserve this tile's range in the scratch output with one atomic (no
+    //     waiting on other tiles); k_scan_tiles + k_reorder restore rank order.
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int w = 0; w < nwarps; w++) {
+            const int64_t c = s_warp_off[w];
+            s_warp_off[w] = acc;
+            acc += c;
+        }
+        const int64_t base = acc ? (int64_t)atomicAdd(fa.alloc, (unsigned long long)acc) : 0;
+        fa.tile_base[tile] = base;
+        fa.tile_cnt[tile] = (int32_t)acc;
+        s_tile_off = base;
+    }
+    __syncthreads();
+    if (fa.out == nullptr) return;
+
+    // (4) ordered emission. Primes are sparse (~0.2 per block at n = 24, ~5
+    //     nonzero blocks per 32-block group), so the nonzero blocks of the
+    //     warp's range are first compacted into a list (ballot + prefix;
+    //     s_cnt is free again), then processed 32 at a time with every lane
+    //     busy: reload the block, popcount, one warp scan for the positions,
+    //     walk the set bits. Stores of one step ascend with the lane and coalesce.
+    const int64_t off = s_tile_off + s_warp_off[warp];
+    uint16_t *lst = &s_cnt[warp][0][0];  // kMaxIter * 32 entries >= the warp's range
+    const uint32_t lt = (1u << lane) - 1u;
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxIter; j++) {
+        const uint32_t c = (pk[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
+        if (c) lst[n + __popc(m & lt)] = (uint16_t)(32 * j + lane);
+        n += __popc(m);
+    }
+    __syncwarp();
+    int64_t run = off;
+#pragma unroll 1
+    for (int e0 = 0; e0 < n; e0 += 32) {
+        const int e = e0 + lane;
+        uint32_t wv[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        int cnt = 0, b = 0;
+        if (e < n) {
+            b = b0 + lst[e];
+            const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+            const uint4 x0 = p[0], x1 = p[1];
+            wv[0] = x0.x, wv[1] = x0.y, wv[2] = x0.z, wv[3] = x0.w;
+            wv[4] = x1.x, wv[5] = x1.y, wv[6] = x1.z, wv[7] = x1.w;
+#pragma unroll
+            for (int k = 0; k < 8; k++) cnt += __popc(wv[k]);
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int64_t pos = run + (incl - cnt);
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+        int64_t *o = fa.out + pos;
+        if (pos + cnt <= fa.cap) {
+            // walk only the nonzero words (most blocks hold one or two): their
+            // mask from the registers, the words themselves re-read from smem
+            uint32_t nz = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) nz |= (wv[k] != 0u ? 1u : 0u) << k;
+            const uint32_t *bw = sm + b * 8;
+            while (nz) {
+                const int k = __ffs(nz) - 1;
+                nz &= nz - 1;
+                uint32_t w = bw[k];
+                do {
+                    *o++ = rbase + k * 32 + (__ffs(w) - 1);
+                    w &= w - 1;
+                } while (w);
+            }
+        } else {  // the scratch is too small: write what fits (the host grows it and reruns)
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                uint32_t w = wv[k];
+                while (w) {
+                    if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                    pos++;
+                    w &= w - 1;
+                }
+            }
+        }
+    }
+}
+
+// Exclusive scan of the per-tile counts (one CTA) -> rank-order positions and
+// the total prime count.
+__global__ void __launch_bounds__(1024) k_scan_tiles(const int32_t *__restrict__ cnt, int64_t *__restrict__ pos,
+                                                     int64_t n, int64_t *total) {
+    __shared__ int64_t s_part[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = min(n, t * per), hi = min(n, lo + per);
+    int64_t acc = 0;
+    for (int64_t i = lo; i < hi; i++) acc += cnt[i];
+    s_part[t] = acc;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int64_t y = t >= o ? s_part[t - o] : 0;
+        __syncthreads();
+        s_part[t] += y;
+        __syncthreads();
+    }
+    int64_t run = s_part[t] - acc;
+    for (int64_t i = lo; i < hi; i++) {
+        pos[i] = run;
+        run += cnt[i];
+    }
+    if (t == blockDim.x - 1) *total = s_part[t];
+}
+
+// chunk pipeline: next = cur + pos[last] + cnt[last] (device-side running base)
+__global__ void k_chunk_advance(const int32_t *__restrict__ cnt_last, const int64_t *__restrict__ pos_last,
+                                int64_t *base, volatile int64_t *host_mirror) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const int64_t b0 = base[0], b1 = b0 + *pos_last + *cnt_last;
+        base[1] = b1;
+        host_mirror[0] = b0;  // mapped pinned memory: the host reads it after the chunk event
+        host_mirror[1] = b1;
+    }
+}
+
+// total = pos[n-1] + cnt[n-1] after the exclusive scan
+__global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos, int64_t n,
+                             int64_t *total) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *total = n ? pos[n - 1] + cnt[n - 1] : 0;
+}
+
+// Copy every tile's ranks from its scratch range to its rank-order position
+// (one warp per tile, coalesced 8-B copies).
+// DQMC_FLAG_ASYNC: publish the count in stream order; -(count + 1) flags an
+// incomplete rank list (output or scratch too small).
+__global__ void k_publish_count(const int64_t *__restrict__ total, int64_t limit, int64_t *__restrict__ dst) {
+    const int64_t t = *total;
+    *dst = t <= limit ? t : -(t + 1);
+}
+
+__global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
+                                                 const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
+                                                 int64_t *__restrict__ out, int64_t cap, int64_t ntiles,
+                                                 int64_t scap, const int64_t *__restrict__ dbase = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t add = dbase ? *dbase : 0;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t t = w; t < ntiles; t += nw) {
+        const int c = cnt[t];
+        const int64_t src = base[t], dst = pos[t] + add;
+        // a tile whose range overflowed the scratch is skipped: the host sees
+        // total > scratch capacity, grows the scratch and reruns the final stage
+        if (c < 0 || src < 0 || src + c > scap) continue;
+        int i = lane;
+        if (dst + c <= cap) {
+            // four independent loads in flight per lane (the copy is latency-bound)
+            for (; i + 96 < c; i += 128) {
+                const int64_t a0 = __ldcs(scratch + src + i), a1 = __ldcs(scratch + src + i + 32);
+                const int64_t a2 = __ldcs(scratch + src + i + 64), a3 = __ldcs(scratch + src + i + 96);
+                out[dst + i] = a0;
+                out[dst + i + 32] = a1;
+                out[dst + i + 64] = a2;
+                out[dst + i + 96] = a3;
+            }
+        }
+        for (; i < c; i += 32)
+            if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
+    }
+}
+
+// REDUCE along C0 axes [J0, J0+K) of a 3^G-block tile, compile-time shape.
+template <int K, int G, int J0>
+__device__ __forceinline__ void tile_reduce_axes_t(uint32_t *sm) {
+    constexpr int N = P3<K>::v;
+    constexpr int SJ = pow3i(J0);
+    constexpr int SPAN = SJ * N;
+    constexpr int NHI = pow3i(G) / SPAN;
+    constexpr int NTASK = SJ * NHI * 8;
+    // warp-uniform iterations: an all-zero warp skips its reduce (see warp_any)
+    for (int t0 = (int)(threadIdx.x & ~31u); t0 < NTASK; t0 += blockDim.x) {
+        const int t = t0 + (int)(threadIdx.x & 31u);
+        const bool in = t < NTASK;
+        const int w = t & 7, q = in ? t >> 3 : 0;
+        const int lo = q % SJ, hi = q / SJ;
+        const int blk = lo + hi * SPAN;
+        uint32_t v[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) v[i] = sm[(blk + i * SJ) * 8 + w];
+        if (K <= 3) {  // 81-register cubes (K = 4) would spill with the vote
+            if (!warp_any(v) || !in) continue;
+        } else if (!in) {
+            continue;
+        }
+        cube_reduce_par<K>(v);
+#pragma unroll
+        for (int i = 0; i < N; i++) sm[(blk + i * SJ) * 8 + w] = v[i];
+    }
+    __syncthreads();
+}
+
+template <int G, int J0>
+__device__ __forceinline__ void tile_reduce_c0_t(uint32_t *sm) {
+    if constexpr (G - J0 == 7) {
+        tile_reduce_axes_t<4, G, J0>(sm);
+        tile_reduce_c0_t<G, J0 + 4>(sm);
+    } else if constexpr (G - J0 >= 3) {
+        tile_reduce_axes_t<3, G, J0>(sm);
+        tile_reduce_c0_t<G, J0 + 3>(sm);
+    } else if constexpr (G - J0 == 2) {
+        tile_reduce_axes_t<2, G, J0>(sm);
+    } else if constexpr (G - J0 == 1) {
+        tile_reduce_axes_t<1, G, J0>(sm);
+    }
+}
+
+// pass E: one CTA per C0 tile (3^G blocks); the tile arrives in shared
+// memory with one TMA bulk copy (or three 4-D tensor boxes, piece-major).
+
+template <int G>
+__global__ void __launch_bounds__(kFinalThreads, 3)
+    k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa, const __grid_constant__ CUtensorMap ma,
+               const __grid_constant__ CUtensorMap mb) {
+    extern __shared__ __align__(128) uint32_t sm_raw[];
+    __shared__ __align__(8) uint64_t mbar;
+    constexpr int NB = pow3i(G);
+    // tensor-map destinations need 128-B alignment; the dynamic window follows
+    // this kernel's static arrays (the launch reserves 128 B for the shift)
+    uint32_t *sm = sm_raw + (fa.pm_nr ? ((128u - (smem_u32(sm_raw) & 127u)) & 127u) >> 2 : 0u);
+    const int64_t tile = blockIdx.x + fa.tile0;
+    const int64_t blk0 = tile * NB;  // logical (rank) block
+    const int64_t pitch = fa.pitch ? fa.pitch : NB;
+    const uint32_t *src = state + tile * pitch * 8;
+    if (threadIdx.x == 0 && fa.pm_nr) {
+        // piece-major group 0: the tile is pm_np pieces 3^r pieces apart; boxes
+        // of 256 pieces (map ma) and one remainder box (map mb)
+        mbar_init(&mbar, 1);
+        mbar_expect_tx(&mbar, fa.pm_np * 128);
+        const int nfull = fa.pm_np >> 8, rem = fa.pm_np & 255;
+        const int q1 = (int)(tile % fa.pm_nr), up = (int)(tile / fa.pm_nr);
+        for (int j = 0; j < nfull; j++) tma_load_4d(sm + j * 256 * 32, &ma, 0, 256 * j, q1, up, &mbar);
+        if (rem) tma_load_4d(sm + nfull * 256 * 32, &mb, 0, 256 * nfull, q1, up, &mbar);
+        const int pf = (int)blockIdx.x + fa.prefetch;
+        if (fa.prefetch > 0 && pf < (int)gridDim.x) {
+            const int64_t t2 = tile + fa.prefetch;
+            const int q1b = (int)(t2 % fa.pm_nr), upb = (int)(t2 / fa.pm_nr);
+            for (int j = 0; j < nfull; j++) tma_prefetch_4d(&ma, 0, 256 * j, q1b, upb);
+            if (rem) tma_prefetch_4d(&mb, 0, 256 * nfull, q1b, upb);
+        }
+    } else if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
+        mbar_expect_tx(&mbar, NB * 32);
+        bulk_g2s(sm, src, NB * 32, &mbar);
+        // warm L2 for the CTA that will take this slot a generation later
+        // (CTAs start roughly in tile order, ~3 per SM resident)
+        const int pf = (int)blockIdx.x + fa.prefetch;
+        if (fa.prefetch > 0 && pf < (int)gridDim.x)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (int64_t)fa.prefetch * pitch * 8),
+                         "r"(NB * 32)
+                         : "memory");
+    }
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    tile_reduce_c0_t<G, 0>(sm);
+    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa);
+}
+
+// n <= 12: the whole problem is one tile; one CTA does A and E.
+__global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restrict__ tt32, int g, FinalArgs fa) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    tile_build(sm, tt32, g, 0);
+    tile_reduce_c0(sm, g);
+    tile_finish<kTileThreads>(sm, (int)pow3l(g), 0, 0, fa);
+}
+
+// E's tensor maps for piece-major group 0: dims {32 words, pieces (3^r x 128 B
+// apart), group-0 rows (128 B apart), upper (pieces x 3^r x 128 B apart)}
+int make_final_maps(const Plan &p, const uint32_t *state, CUtensorMap *ma, CUtensorMap *mb, FinalArgs &fa) {
+    memset(ma, 0, sizeof *ma);
+    memset(mb, 0, sizeof *mb);
+    fa.pm_nr = 0;
+    fa.pm_np = 0;
+    if (!p.pm) return DQMC_OK;
+    int rc;
+    if ((rc = ensure_encode())) return rc;
+    const int64_t nr = pow3l(p.r[0]), np = p.pitch / kRowBlocks, nu = pow3l(p.T - p.r[0]);
+    cuuint64_t dims[4] = {32, (cuuint64_t)np, (cuuint64_t)nr, (cuuint64_t)nu};
+    cuuint64_t strides[3] = {(cuuint64_t)(nr * 128), 128, (cuuint64_t)(np * nr * 128)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    for (int k = 0; k < 2; k++) {
+        const int rows = k == 0 ? 256 : (int)(np & 255);
+        if (rows == 0) continue;
+        cuuint32_t box[4] = {32, (cuuint32_t)rows, 1, 1};
+        CUresult r = g_eng.encode(k == 0 ? ma : mb, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (void *)state, dims, strides, box,
+                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (final) failed: " + std::to_string((int)r));
+    }
+    fa.pm_nr = (int)nr;
+    fa.pm_np = (int)np;
+    return DQMC_OK;
+}
+
+int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArgs &fa, const CUtensorMap &ma,
+                    const CUtensorMap &mb, cudaStream_t s) {
+    const int smem = fa.pm_nr ? fa.pm_np * 128 + 128 : (int)pow3l(g) * 32;
+    switch (g) {
+#define CASE(G)                                                                         \
+    case G:                                                                             \
+        k_c0_final<G><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);  \
+        break;
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+        default: return set_err(DQMC_ERR_INVALID, "bad tile exponent");
+    }
+    CK(cudaGetLastError());
+    return DQMC_OK;
+}
+
+// Final stage: E (+ scan + reorder). Source: the truth table (k_small, fused
+// A+E, when tt32 != null) or a merged/reduced state. Returns the prime count.
+}  // namespace
+
+int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32_t ib_mask, int64_t rank_add,
+              int64_t *ranks, int64_t cap, bool count_only, const FinalOpts &o, int64_t *count, Timer &tm,
+              cudaStream_t s) {
+    uint32_t *bitmap_out = o.bitmap_out;
+    int64_t *count_dev = o.count_dev;
+    if (o.nkill < 0 || o.nkill > kMaxKill) return set_err(DQMC_ERR_INVALID, "too many kill bitmaps");
+    const uint64_t S = (uint64_t)p.nblocks * 32;
+    const int64_t ntiles = p.T == 0 ? 1 : pow3l(p.T);
+    const int tile_smem = (int)pow3l(p.g) * 32;
+    int rc;
+    if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    if ((o.nkill || bitmap_out) && p.T > 0 && p.pitch != pow3l(p.g))
+        return set_err(DQMC_ERR_INVALID, "internal: kill/bitmap outputs need the reference layout plan");
+    const bool direct = ntiles == 1;  // one tile: its ranks are already in order
+    if (!count_only && !direct) {
+        const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+    }
+    FinalArgs fa;
+    fa.out = count_only ? nullptr : (direct ? ranks : g_eng.scratch);
+    fa.cap = count_only ? 0 : (direct ? cap : (int64_t)g_eng.scratch_cap);
+    fa.rank_add = rank_add;
+    fa.nkill = o.nkill;
+    for (int q = 0; q < o.nkill; q++) fa.kill[q] = o.kill[q];
+    fa.ib_mask = ib_mask;
+    fa.bitmap_out = bitmap_out;
+    fa.alloc = g_eng.alloc;
+    fa.tile_base = g_eng.tile_base;
+    fa.tile_cnt = g_eng.tile_cnt;
+    fa.tile0 = 0;
+    fa.pitch = p.pitch;
+    fa.prefetch = 3 * g_eng.num_sms;  // one generation of resident CTAs (3 per SM): 9.23 -> 9.0 ms at n=24
+    CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
+    if (tt32) {
+        k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
+        CK(cudaGetLastError());
+        tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (bitmap_out ? S : 0));
+    } else {
+        CUtensorMap ma, mb;
+        if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
+        if ((rc = launch_c0_final(p.g, ntiles, state, fa, ma, mb, s))) return rc;
+        tm.mark("k_c0_final", S * (1 + o.nkill) + (bitmap_out ? S : 0));
+    }
+    if (ntiles <= 4096) {
+        k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
+        CK(cudaGetLastError());
+    } else {
+        // device-wide exclusive scan (CUB) of the int32 counts into int64 positions
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int64_t)ntiles, s));
+        if ((rc = grow(g_eng.cub_tmp, g_eng.cub_tmp_cap, tmp, 1))) return rc;
+        CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int64_t)ntiles, s));
+        k_scan_total<<<1, 32, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
+        CK(cudaGetLastError());
+    }
+    tm.mark("k_scan_tiles", (uint64_t)ntiles * 12);
+    if (!count_only && !direct) {
+        const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
+        k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos, ranks, cap,
+                                       ntiles, (int64_t)g_eng.scratch_cap);
+        CK(cudaGetLastError());
+        tm.mark("k_reorder", (uint64_t)ntiles * 16);
+    }
+    if (count_dev) {  // DQMC_FLAG_ASYNC: no host synchronisation
+        const int64_t limit = count_only ? INT64_MAX : (direct ? cap : std::min<int64_t>(cap, (int64_t)g_eng.scratch_cap));
+        k_publish_count<<<1, 1, 0, s>>>(g_eng.total, limit, count_dev);
+        CK(cudaGetLastError());
+        return DQMC_OK;
+    }
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, g_eng.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *count = total;
+    return DQMC_OK;
+}
+
+namespace {
+void add_rank_bytes(Timer &tm, int64_t written) {
+    if (tm.bytes.empty()) return;
+    for (size_t i = 0; i < tm.names.size(); i++) {
+        if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += (uint64_t)written * 8;
+        if (tm.names[i] == "k_reorder") tm.bytes[i] += (uint64_t)written * 16;
+    }
+}
+}  // namespace
+
+// Final stage with the scratch-regrow retry (the stage does not modify the
+// merged state it reads; with a bitmap output it rewrites the same P).
+int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32_t ib_mask, int64_t rank_add,
+                    int64_t *ranks, int64_t cap, bool count_only, const FinalOpts &o, int64_t *count, Timer &tm,
+                    cudaStream_t s) {
+    int rc;
+    if ((rc = run_final(p, tt32, state, ib_mask, rank_add, ranks, cap, count_only, o, count, tm, s))) return rc;
+    if (o.count_dev) return DQMC_OK;  // async: the caller sees -(count + 1) and retries synchronously
+    const bool direct = (p.T == 0);
+    if (!count_only && !direct && (size_t)*count > g_eng.scratch_cap) {
+        g_eng.scratch_want = (size_t)((double)*count * 1.05) + 1024;
+        const bool on = tm.on;
+        tm.on = false;
+        FinalOpts o2 = o;
+        o2.count_dev = nullptr;
+        rc = run_final(p, tt32, state, ib_mask, rank_add, ranks, cap, count_only, o2, count, tm, s);
+        tm.on = on;
+        if (rc) return rc;
+    }
+    if (!count_only) add_rank_bytes(tm, std::min<int64_t>(*count, cap));
+    return DQMC_OK;
+}
+
+// Host-API final stage, pipelined: the tiles are finished in K chunks on the
+// compute stream (E, scan, running base, reorder into the device rank
+// buffer); as soon as chunk c's event fires the host queues its D2H copy on
+// the copy stream, so the copy engine moves chunk c while the SMs finish
+// chunk c+1. Returns the total; *host_ok is false if the host buffer (sized
+// from the previous call) was too small.
+int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int64_t host_cap, int64_t *count,
+                        bool *host_ok, cudaStream_t s) {
+    const int64_t ntiles = pow3l(p.T);
+    const int K = (int)std::min<int64_t>(16, ntiles);
+    int rc;
+    if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
+    if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
+    if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)host_cap, 8))) return rc;
+    int64_t *hbase = g_eng.hbase;  // mapped pinned mirror of the chunk bases
+    for (int attempt = 0; attempt < 2; attempt++) {
+        const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+        FinalArgs fa;
+        fa.out = g_eng.scratch;
+        fa.cap = (int64_t)g_eng.scratch_cap;
+        fa.rank_add = -p.rank_sub;
+        fa.ib_mask = p.ib_E;
+        fa.bitmap_out = nullptr;
+        fa.alloc = g_eng.alloc;
+        fa.tile_base = g_eng.tile_base;
+        fa.tile_cnt = g_eng.tile_cnt;
+        fa.prefetch = 3 * g_eng.num_sms;
+        fa.pitch = p.pitch;
+        CUtensorMap ma, mb;
+        if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
+        CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
+        CK(cudaMemsetAsync(g_eng.chunk_base, 0, 8, s));
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
+                                          (int)((ntiles + K - 1) / K + 1), s));
+        if ((rc = grow(g_eng.cub_tmp, g_eng.cub_tmp_cap, tmp, 1))) return rc;
+        for (int c = 0; c < K; c++) {
+            const int64_t t0 = ntiles * c / K, t1 = ntiles * (c + 1) / K;
+            fa.tile0 = t0;
+            if ((rc = launch_c0_final(p.g, t1 - t0, state, fa, ma, mb, s))) return rc;
+            CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt + t0, g_eng.tile_pos + t0, cub::Sum(),
+                                              (int64_t)0, (int64_t)(t1 - t0), s));
+            k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c,
+                                             hbase + c);
+            CK(cudaGetLastError());
+            const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 8);
+            k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
+                                           g_eng.tile_pos + t0, g_eng.ranks, host_cap, t1 - t0,
+                                           (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(g_eng.chunk_ev[c], s));
+        }
+        // copy-out as chunks complete (copy engine, overlapped with later chunks)
+        bool fits = true;
+        for (int c = 0; c < K; c++) {
+            CK(cudaEventSynchronize(g_eng.chunk_ev[c]));
+            const int64_t lo = hbase[c], hi = hbase[c + 1];
+            if (hi > host_cap) fits = false;
+            if (fits && hi > lo)
+                CK(cudaMemcpyAsync(host + lo, g_eng.ranks + lo, (size_t)(hi - lo) * 8, cudaMemcpyDeviceToHost,
+                                   g_eng.stream2));
+        }
+        int64_t used = 0;
+        CK(cudaMemcpyAsync(&used, g_eng.alloc, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(g_eng.stream2));
+        *count = hbase[K];
+        *host_ok = fits && *count <= host_cap;
+        if ((size_t)used <= g_eng.scratch_cap) break;
+        g_eng.scratch_want = (size_t)((double)used * 1.05) + 1024;  // scratch overflow: once more
+    }
+    return DQMC_OK;
+}
+
+int final_set_attrs() {
+    const int tile_smem = (int)pow3l(kC0Max) * 32;
+    // + one 128-B piece (the padded pitch of a piece-major tile, make_plan) + 128 B of alignment
+    CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem + 256));
+    CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    return DQMC_OK;
+}
+
+}  // namespace dqmc

@@ -329,9 +329,9 @@ int dqmc_state_extract(const dqmc_state_t *st, int64_t *ranks_host, int64_t cap,
     SCK(cudaMalloc(&bad, 4));
     SCK(cudaMemset(bad, 0, 4));
     k_state_count<<<grid_for(st->nw), 256>>>(st->words, st->nw, st->wpb, st->used, cnt, bad);
-    SCK(cub::DeviceScan::ExclusiveScan(nullptr, tmpb, cnt, pos, cub::Sum(), (int64_t)0, (int)st->nw));
+    SCK(cub::DeviceScan::ExclusiveScan(nullptr, tmpb, cnt, pos, cub::Sum(), (int64_t)0, (int64_t)st->nw));
     SCK(cudaMalloc(&tmp, tmpb));
-    SCK(cub::DeviceScan::ExclusiveScan(tmp, tmpb, cnt, pos, cub::Sum(), (int64_t)0, (int)st->nw));
+    SCK(cub::DeviceScan::ExclusiveScan(tmp, tmpb, cnt, pos, cub::Sum(), (int64_t)0, (int64_t)st->nw));
     int hb = 0;
     int64_t lastpos = 0;
     int32_t lastcnt = 0;

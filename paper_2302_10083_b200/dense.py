@@ -179,8 +179,8 @@ def count_primes(tt: TruthTable, mem_cap: int | None = None) -> int:
     n, words = _as_words(tt)
     L = _lib.load()
     res = _lib.DqmcResult()
-    rc = L.dqmc_primes_tt(words.ctypes.data, n, 0, 0 if mem_cap is None else int(mem_cap), _lib.FLAG_COUNT_ONLY,
-                          ctypes.byref(res))
+    cap = _cap_arg(n, 0, mem_cap)
+    rc = L.dqmc_primes_tt(words.ctypes.data, n, 0, cap, _lib.FLAG_COUNT_ONLY, ctypes.byref(res))
     _lib.check(rc)
     cnt = int(res.count)
     L.dqmc_free_result(ctypes.byref(res))

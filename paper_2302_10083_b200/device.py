@@ -100,11 +100,24 @@ class PrimesGraph:
         torch.cuda.current_stream(table.device).wait_stream(s)
         torch.cuda.synchronize(table.device)
         self.graph = torch.cuda.CUDAGraph()
+        L = _lib.load()
         with torch.cuda.graph(self.graph, stream=s):
             enqueue_prime_ranks(table, n, self.out, self.count)
+        # the graph holds raw pointers into the engine workspace: valid until
+        # the engine reallocates or releases a buffer (dqmc_engine_generation)
+        self.generation = int(L.dqmc_engine_generation())
 
     def replay(self) -> None:
+        """Launch the captured call on the current stream, ordered after every
+        earlier use of the engine workspace and before every later one."""
+        L = _lib.load()
+        if int(L.dqmc_engine_generation()) != self.generation:
+            raise RuntimeError("the engine workspace was reallocated or released since this graph was captured; "
+                               "build a new PrimesGraph")
+        stream = torch.cuda.current_stream(self.table.device).cuda_stream
+        _lib.check(L.dqmc_engine_enter(stream))
         self.graph.replay()
+        _lib.check(L.dqmc_engine_exit(stream))
 
     def ranks(self) -> torch.Tensor:
         c = int(self.count.item())

@@ -42,7 +42,7 @@ def test_abi_version_and_sizes(pkg):
     from paper_2302_10083_b200 import _lib
 
     L = _lib.load()
-    assert L.dqmc_abi_version() == 1
+    assert L.dqmc_abi_version() == 2
     for h in range(1, 10):
         assert L.dqmc_block_bits(h) == pkg.block_bits_for(h)
     for n in range(1, 28):
@@ -112,3 +112,12 @@ def test_ternary_helpers(pkg):
     assert pkg.unrank_many(np.array([14, 16, 22]), 3) == ["*11", "1*1", "11*"]
     assert pkg.ranks_to_text(np.array([14]), 3, wildcard="-") == "-11\n"
     assert pkg.rank_weights(np.array([26, 0]), 3).tolist() == [3, 0]
+
+
+def test_count_primes_cap_validated_like_load(pkg):
+    # dense.py:358-364: a cap that cannot hold the state raises before any
+    # allocation (0 and negative caps included), naming the bytes
+    tt = pkg.TruthTable.full(12)
+    for cap in (0, -5):
+        with pytest.raises(pkg.ResourceLimitError, match=str(pkg.state_bytes(12, 5))):
+            pkg.count_primes(tt, mem_cap=cap)

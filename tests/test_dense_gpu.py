@@ -347,3 +347,57 @@ class TestJobStream:
             b.result()  # out of order
         ra, rb, rc = a.result(), b.result(), c.result()
         assert np.array_equal(ra, rb) and np.array_equal(ra, rc) and np.array_equal(ra, pkg.prime_ranks_from_values(t))
+
+
+class TestWorkspaceSafety:
+    """Entry points sharing the engine workspace stay ordered, and captured
+    graphs refuse to replay over reallocated buffers."""
+
+    def test_graph_refuses_after_release(self, pkg):
+        from paper_2302_10083_b200 import _lib, device
+
+        v = device.gen3_device(16, 0.7, 0.05, 4)
+        g = device.PrimesGraph(v, 16)
+        g.replay()
+        _lib.load().dqmc_release()
+        with pytest.raises(RuntimeError, match="reallocated or released"):
+            g.replay()
+
+    def test_jobs_and_device_calls_interleaved(self, pkg, gen_mod):
+        import torch
+        from paper_2302_10083_b200 import device
+
+        n = 18
+        tabs = [gen_mod.gen3(n, 0.7, 0.05, s) for s in (11, 12, 13)]
+        want = [pkg.prime_ranks_from_values(t) for t in tabs]
+        dv = device.gen3_device(n, 0.6, 0.1, 21)
+        dref, dcnt = device.dense_prime_ranks_device(dv, n)
+        dref = dref.clone()
+        jobs = [pkg.submit(t) for t in tabs]  # three jobs queued on the host-API stream
+        out = torch.empty(dcnt + 64, dtype=torch.int64, device="cuda")
+        c = torch.zeros(1, dtype=torch.int64, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):  # a caller-stream call while the jobs are in flight
+            device.enqueue_prime_ranks(dv, n, out, c)
+        got = [j.result() for j in jobs]
+        s.synchronize()
+        assert int(c.item()) == dcnt and torch.equal(out[:dcnt], dref)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+    def test_bitmap_dropped_by_later_calls(self, pkg, gen_mod):
+        t = pkg.TruthTable(16, gen_mod.random_words(16, 0.6, 3))
+        bm = pkg.prime_bitmap(t)
+        assert bm.any()
+        # a host call on the pipelined path (count hint present) reuses the state
+        pkg.dense_prime_ranks(t)
+        pkg.dense_prime_ranks(t)
+        with pytest.raises(ValueError, match="no bitmap held"):
+            _download_only(pkg)
+
+
+def _download_only(pkg):
+    from paper_2302_10083_b200 import _lib
+
+    out = np.zeros(pkg.state_bytes(16, 5) // 8, dtype=np.uint64)
+    _lib.check(_lib.load().dqmc_bitmap_download(out.ctypes.data, out.nbytes))
