@@ -18,10 +18,21 @@ inputs from the reference's frozen generator.
          synchronous prime_ranks_from_values call.
   roofline  the dominant kernel's algorithmic bytes per launch / its
          CUDA-event duration vs MEASURED_PEAKS.json hbm_gbs.
+  configs  BASELINE configs 1-3 (n = 10, 16, 20): wall time to all prime
+         implicants through the drop-in call (t_api: host table -> host int64
+         ranks) and device-resident (t_device), each with the CPU times beside
+         it: the oracle port on 1 thread and on all threads, and the reference
+         package itself (implicants.dense_prime_ranks, 1 thread) when it is
+         installed in baseline/_ref.
   cpu_baseline  the oracle port (C restatement of the reference's dense
-         engine, all host threads) on a bounded sample of the same workload.
+         engine, all host threads) on a bounded sample of the same workload,
+         with the host CPU model and core count, the reference package's own
+         time at n=21 as a cross-check of the port, and the one-off 1-thread
+         n=24 measurement (profiles/r2_cpu_n24.json, tools/cpu_n24.py).
 
---impl reference times that CPU implementation alone (the reference arm).
+--impl reference times the reference's CPU path (the oracle port, all host
+threads) on the SAME workload as our arm: full n=24 config-4 calls, one per
+step (the step count is capped by a time budget; see run_reference).
 Under torchrun (N>1) the engine runs sharded on the top log2(N) variables
 (paper_2302_10083_b200.sharded); the reference arm runs on rank 0 only.
 """
@@ -42,6 +53,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 WORKLOAD = dict(n=24, p_on=0.75, p_dc=0.05, seed=3)  # BASELINE config 4
+WORKLOAD_NAME = "BASELINE config 4: n=24, P(on)=0.75, P(dc)=0.05, seed 3, all primes as int64 ranks"
 E2E_MIN_CALLS = 30  # calls per timed job-stream batch (fill + drain amortised)
 METRIC = "ternary cells/s to all prime implicants"
 UNIT = "cells/s"
@@ -127,54 +139,158 @@ class ClockSampler:
         }
 
 
-def cpu_port_run(n: int, threads: int = 0) -> tuple[float, int, int]:
+def cpu_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem = None
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable"):
+                    mem = int(line.split()[1]) * 1024
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_available_bytes": mem}
+
+
+def config_values_cpu(cfg: int):
+    """uint8 values of a BASELINE config from the oracle's generator (CPU leg)."""
+    from oracle import gen as G
+
+    return G.config_values(cfg)
+
+
+def cpu_port_run(n: int, threads: int = 0, values=None) -> tuple[float, int, int]:
     """Oracle port (C restatement of dense.py) on the host cores: (seconds, primes, threads)."""
     from oracle import gen as G
     from oracle import oracle as O
 
     O.build()
     t = O.set_threads(threads if threads > 0 else (os.cpu_count() or 1))
-    w = G.values_to_words(G.gen3(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"]))
+    v = values if values is not None else G.gen3(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"])
+    w = G.values_to_words(v)
     t0 = time.perf_counter()
     r = O.dense_prime_ranks(w, n)
     dt = time.perf_counter() - t0
+    if values is None:
+        _PORT_PRIMES[n] = len(r)
     return dt, len(r), t
 
 
+_PORT_PRIMES: dict = {}  # n -> prime count of the last port run on the config-4 distribution
+REF_PKG = os.path.join(REPO, "baseline", "_ref")
+_REF_TIMER = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(1, sys.argv[2])
+from implicants import TruthTable, dense_prime_ranks
+from oracle import gen as G
+out = {}
+for spec in json.loads(sys.argv[3]):
+    v = G.config_values(spec["cfg"], spec.get("n"))
+    n = len(v).bit_length() - 1
+    tt = TruthTable.from_bools(n, v != 0)
+    best, cnt = None, 0
+    for _ in range(spec["reps"]):
+        t0 = time.perf_counter()
+        r = dense_prime_ranks(tt)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+        cnt = len(r)
+    out[spec["key"]] = {"n": n, "seconds": best, "primes": cnt}
+print(json.dumps(out))
+"""
+
+
+def reference_numpy_times(specs: list[dict]) -> dict | None:
+    """implicants.dense_prime_ranks itself (the reference package, NumPy, one
+    thread as it is written) from baseline/_ref, in a subprocess: min over reps
+    of perf_counter around the call only (bench.py:125,136-158 of the
+    reference). None when the package is not installed there."""
+    import subprocess
+
+    if not os.path.isdir(os.path.join(REF_PKG, "implicants")):
+        return None
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-c", _REF_TIMER, REF_PKG, REPO, json.dumps(specs)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip().splitlines()[-1] if r.stderr.strip() else f"rc={r.returncode}"}
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def one_thread_n24():
+    """The one-off 1-thread n=24 measurement of the port (tools/cpu_n24.py)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_cpu_n24.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+REF_STEP_BUDGET_S = 300.0  # timed reference steps stop once this much CPU time has elapsed
+
+
 def run_reference(args):
+    """The reference arm: the reference's CPU path for this workload — the
+    oracle port (C restatement of dense.py; the reference itself is Python
+    and is timed beside it in our arm's configs/cpu_baseline) — on all host
+    threads, on OUR arm's workload (full n=24 config-4 calls, same metric).
+    One warm-up call at most (a CPU call has nothing to warm beyond the page
+    cache), then up to --steps timed calls, stopping early once
+    REF_STEP_BUDGET_S has elapsed (steps = the calls actually timed)."""
     rank, world, _ = dist_info()
     if rank != 0:
         return 0
-    n_s = args.cpu_sample_n
-    for _ in range(args.warmup):
-        cpu_port_run(n_s)
+    n = args.n
+    info = cpu_info()
+    from oracle import gen as G
+
+    v = G.gen3(n, WORKLOAD["p_on"], WORKLOAD["p_dc"], WORKLOAD["seed"])
+    for _ in range(min(args.warmup, 1)):
+        cpu_port_run(n, values=v)
     times, cnt, thr = [], 0, 1
+    t_start = time.perf_counter()
     for _ in range(args.steps):
-        dt, cnt, thr = cpu_port_run(n_s)
+        dt, cnt, thr = cpu_port_run(n, values=v)
         times.append(dt)
+        if time.perf_counter() - t_start > REF_STEP_BUDGET_S:
+            break
     t = sum(times) / len(times)
-    value = 3**n_s / t
+    value = 3**n / t
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
         "n_gpus": args.gpus,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": len(times),
+        "steps_requested": args.steps,
+        "warmup": min(args.warmup, 1),
         "ms_per_step": t * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic (seeded frozen generator, SURVEY.md §8(d))",
-        "config": {"workload": "BASELINE config 4 (n=24, p_on=0.75, p_dc=0.05, seed=3)", "sample_n": n_s},
+        "config": {"workload": WORKLOAD_NAME, "n": n, "primes": cnt, "same_config": n == WORKLOAD["n"]},
         "cpu_baseline": {
             "value": value,
             "unit": UNIT,
             "cores": thr,
             "kind": "port",
-            "sample": f"n={n_s} of the config-4 distribution ({3**n_s} cells, {cnt} primes) per step",
+            "sample": f"the full n={n} config-4 call per step ({3**n} cells, {cnt} primes); "
+                      f"{len(times)} timed calls (budget {REF_STEP_BUDGET_S:.0f} s)",
+            **info,
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -194,6 +310,74 @@ def load_ncu_traffic(kernel: str):
     except Exception:
         pass
     return None
+
+
+def cpu_port_primes(n: int) -> int | None:
+    return _PORT_PRIMES.get(n)
+
+
+def bench_configs(args, pkg, device, _lib) -> dict:
+    """Configs 1-3: t_api = dense_prime_ranks(TruthTable) host to host (the
+    reference's clock placement, bench.py:136-138 of the reference), and
+    t_device = device-resident table to device ranks; min over reps. Beside
+    them the CPU: oracle port on 1 thread and on all threads, and the
+    reference package (NumPy, 1 thread) if installed in baseline/_ref."""
+    import torch
+
+    from paper_2302_10083_b200 import configs as C
+
+    reps = {1: 20, 2: 10, 3: 5}
+    out = {}
+    for cfg in (1, 2, 3):
+        n = C.CONFIGS[cfg]["n"]
+        vd = C.config_values_device(cfg)
+        hv = vd.cpu().numpy()
+        tt = pkg.TruthTable.from_values(n, hv)
+        r = pkg.dense_prime_ranks(tt)  # warm (sizes the engine for n)
+        primes = len(r)
+        t_api = []
+        for _ in range(reps[cfg]):
+            t0 = time.perf_counter()
+            r = pkg.dense_prime_ranks(tt)
+            t_api.append(time.perf_counter() - t0)
+        assert len(r) == primes
+        outd = torch.empty(primes + 1024, dtype=torch.int64, device=vd.device)
+        device.dense_prime_ranks_device(vd, n, out=outd)
+        t_dev = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(reps[cfg]):
+            torch.cuda.synchronize()
+            e0.record()
+            device.dense_prime_ranks_device(vd, n, out=outd)
+            e1.record()
+            torch.cuda.synchronize()
+            t_dev.append(e0.elapsed_time(e1) / 1e3)
+        d = {"n": n, "primes": primes, "t_api_ms": min(t_api) * 1e3, "t_device_ms": min(t_dev) * 1e3,
+             "cells_per_s_api": 3**n / min(t_api), "cells_per_s_device": 3**n / min(t_dev)}
+        if not args.no_cpu:
+            v = config_values_cpu(cfg)
+            dt1, c1, _ = cpu_port_run(n, threads=1, values=v)
+            dta, ca, tha = cpu_port_run(n, values=v)
+            assert c1 == ca == primes, (cfg, c1, ca, primes)
+            d["cpu_port_1thread_ms"] = dt1 * 1e3
+            d["cpu_port_all_ms"] = dta * 1e3
+            d["cpu_port_threads"] = tha
+        out[str(cfg)] = d
+    if not args.no_cpu:
+        ref = reference_numpy_times([{"key": str(c), "cfg": c, "reps": {1: 5, 2: 3, 3: 1}[c]} for c in (1, 2, 3)])
+        for c in ("1", "2", "3"):
+            if ref is None:
+                out[c]["reference_numpy_ms"] = None
+            elif c in ref:
+                out[c]["reference_numpy_ms"] = ref[c]["seconds"] * 1e3
+                out[c]["reference_numpy_primes_match"] = ref[c]["primes"] == out[c]["primes"]
+            else:
+                out[c]["reference_numpy_ms"] = ref
+    out["note"] = ("t_api: dense_prime_ranks(TruthTable) host to host; t_device: device-resident table to "
+                   "device ranks (CUDA events); CPU: oracle port (C restatement, 1 thread / all threads) and "
+                   "the reference package itself (implicants.dense_prime_ranks, NumPy, 1 thread) from "
+                   "baseline/_ref; min over reps")
+    return out
 
 
 def run_engine_bench(args):
@@ -271,12 +455,17 @@ def run_engine_bench(args):
     for _ in range(max(1, args.warmup)):
         res = pkg.prime_ranks_from_values(hv)
         del res
-    # single synchronous call: latency of one table, host to host
+    # single synchronous drop-in call: dense_prime_ranks(tt) on the reference's
+    # TruthTable layout (host uint64 words in, host int64 ranks out)
+    tt = pkg.TruthTable.from_values(n, hv)
+    for _ in range(max(1, args.warmup)):
+        del_ = pkg.dense_prime_ranks(tt)
+        del del_
     e2e_times = []
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = pkg.prime_ranks_from_values(hv)
+        res = pkg.dense_prime_ranks(tt)
         e2e_times.append(time.perf_counter() - t0)
         assert len(res) == cnt
         del res
@@ -299,6 +488,10 @@ def run_engine_bench(args):
         del r
     t_e2e = (time.perf_counter() - t0) / got
 
+    # ---- BASELINE configs 1-3: wall time to all primes at n (the metric's
+    #      second half), GPU beside the CPU
+    configs = bench_configs(args, pkg, device, _lib)
+
     # ---- CPU baseline: oracle port on a bounded sample (rank 0, N=1)
     cpu = None
     if not args.no_cpu:
@@ -308,8 +501,18 @@ def run_engine_bench(args):
             "unit": UNIT,
             "cores": thr,
             "kind": "port",
-            "sample": f"n={args.cpu_sample_n} of the config-4 distribution ({3**args.cpu_sample_n} cells, {ccnt} primes), one run",
+            "sample": f"n={args.cpu_sample_n} of the config-4 distribution ({3**args.cpu_sample_n} cells, "
+                      f"{ccnt} primes), one run",
+            **cpu_info(),
         }
+        ref = reference_numpy_times([{"key": "n21", "cfg": 4, "n": 21, "reps": 1}])
+        if ref and "n21" in ref:
+            r21 = ref["n21"]
+            cpu["reference_numpy_n21"] = {**r21, "cells_per_s": 3**21 / r21["seconds"], "threads": 1,
+                                          "primes_match_port": r21["primes"] == cpu_port_primes(21)}
+        elif ref is not None:
+            cpu["reference_numpy_n21"] = ref
+        cpu["one_thread_n24"] = one_thread_n24()
 
     traffic = load_ncu_traffic(dom)
     line = {
@@ -321,12 +524,12 @@ def run_engine_bench(args):
         "warmup": args.warmup,
         "ms_per_step": t_step * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic (seeded frozen generator, SURVEY.md §8(d)); generated on device",
         "config": {
-            "workload": "BASELINE config 4: n=24, P(on)=0.75, P(dc)=0.05, seed 3, all primes as int64 ranks",
+            "workload": WORKLOAD_NAME,
             "n": n,
             "cells": 3**n,
             "primes": cnt,
@@ -346,7 +549,7 @@ def run_engine_bench(args):
             "single_call": {
                 "value": 3**n / t_single,
                 "ms": t_single * 1e3,
-                "api": "paper_2302_10083_b200.prime_ranks_from_values (C ABI dqmc_primes_u8)",
+                "api": "paper_2302_10083_b200.dense_prime_ranks(TruthTable) (C ABI dqmc_primes_tt), the drop-in call",
             },
         },
         "roofline": {
@@ -371,6 +574,7 @@ def run_engine_bench(args):
         "all_passes_gbs": all_bytes / (all_ms / 1e3) / 1e9,
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "configs": configs,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -386,7 +590,15 @@ def main():
     ap.add_argument("--nvars", dest="n", type=int, default=WORKLOAD["n"], help="variable count (default: config 4, n=24)")
     ap.add_argument("--cpu-sample-n", type=int, default=21)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="print the sharded plan's per-rank device byte budget for --gpus/--nvars and exit")
     args = ap.parse_args()
+    if args.dry_run:
+        from paper_2302_10083_b200 import sharded
+
+        k = max(1, args.gpus).bit_length() - 1
+        print(json.dumps(sharded.dry_run(args.n, k)), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     return run_engine_bench(args)

@@ -207,6 +207,14 @@ int dqmc_ipc_get(const void *dev_ptr, void *handle_out, uint64_t *offset_out);
 int dqmc_ipc_open(const void *handle, void **base_out);
 int dqmc_ipc_close(void *base);
 
+/* The sparse engine (sparse_prime_ranks, sparse.py:288-307) on the GPU: the
+ * level walk over device hash sets of packed cubes (csrc/dqmc_sparse.cu).
+ * Same output contract as dqmc_primes_tt; mem_cap bounds every level table
+ * (0 = 75% of free device memory), refused before allocating with the
+ * reference's message (sparse.py:105-111). Work scales with the implicant
+ * count, not 3^n: the engine for low-density functions. */
+int dqmc_sparse_primes_tt(const uint64_t *tt_words, int n, uint64_t mem_cap, dqmc_result_t *out);
+
 /* The pass plan the engine runs for n variables (host logic, no GPU needed):
  * out = {ne, H, g, T, m, r[0..7], a[0..7], ib_C, ib_E, ib_D[0..7], rank_sub}
  * (32 int64 entries). Returns the number written. */

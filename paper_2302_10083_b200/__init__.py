@@ -22,6 +22,7 @@ from .dense import (
     submit,
 )
 from .engine import ENGINES, run_engine
+from .sparse import find_primes_sparse, sparse_prime_ranks
 from .errors import ImplicantsError, ParseError, ResourceLimitError
 from .ternary import (
     MAX_N,
@@ -54,6 +55,7 @@ __all__ = [
     "count_primes",
     "dense_prime_ranks",
     "find_primes_dense",
+    "find_primes_sparse",
     "index_to_rank",
     "prime_bitmap",
     "prime_ranks_from_values",
@@ -63,6 +65,7 @@ __all__ = [
     "ranks_to_text",
     "run_engine",
     "stream_prime_ranks",
+    "sparse_prime_ranks",
     "submit",
     "state_bytes",
     "unrank",

@@ -13,7 +13,7 @@ import threading
 
 import numpy as np
 
-from .errors import ResourceLimitError
+from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdqmc.so")
@@ -69,6 +69,7 @@ EXPORTS = (
     "dqmc_engine_generation",
     "dqmc_engine_enter",
     "dqmc_engine_exit",
+    "dqmc_sparse_primes_tt",
     "dqmc_state_create",
     "dqmc_state_free",
     "dqmc_state_info",
@@ -167,6 +168,7 @@ def load() -> ctypes.CDLL:
             "dqmc_engine_generation": (u64, []),
             "dqmc_engine_enter": (i32, [vp]),
             "dqmc_engine_exit": (i32, [vp]),
+            "dqmc_sparse_primes_tt": (i32, [vp, i32, u64, ctypes.POINTER(DqmcResult)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -189,7 +191,7 @@ def check(rc: int) -> None:
     if rc == DQMC_ERR_INVALID:
         raise ValueError(msg)
     if rc == DQMC_ERR_RESOURCE:
-        raise ResourceLimitError(msg)
+        raise errors.ResourceLimitError(msg)
     if rc == DQMC_ERR_NODEVICE:
         raise RuntimeError(f"CUDA device required: {msg}")
     raise RuntimeError(f"libdqmc CUDA error: {msg}")

@@ -37,7 +37,7 @@ import numpy as np
 
 from . import _lib
 from .dense import dense_prime_ranks, prime_ranks_from_values
-from .errors import ParseError, ResourceLimitError
+from . import errors
 from .ternary import TruthTable, ranks_to_text
 
 _CORRUPT_ENV = "IMPLICANTS_VERIFY_CORRUPT"  # same fault-injection hook as cli.py:40-42
@@ -65,10 +65,10 @@ def read_bits(text: str) -> TruthTable:
     """The reference's 'bits' format (ttio.py:1-20): n from the length."""
     bits = "".join(text.split())
     if not bits or any(c not in "01" for c in bits):
-        raise ParseError("bits format expects only '0'/'1' characters")
+        raise errors.ParseError("bits format expects only '0'/'1' characters")
     n = len(bits).bit_length() - 1
     if len(bits) != 1 << n or n < 1:
-        raise ParseError(f"bits format needs 2^n characters, got {len(bits)}")
+        raise errors.ParseError(f"bits format needs 2^n characters, got {len(bits)}")
     return TruthTable.from_bools(n, np.frombuffer(bits.encode(), dtype=np.uint8) == ord("1"))
 
 
@@ -100,7 +100,7 @@ def _input(args):
         v = config_values_host(args.config, args.n)
         return (args.n or CONFIGS[args.config]["n"]), None, v
     if args.n is None or args.density is None:
-        raise ParseError("provide --input PATH, --config K, or both --n and --density to generate")
+        raise errors.ParseError("provide --input PATH, --config K, or both --n and --density to generate")
     v = generate_values(args.n, args.density, args.seed, args.dc)
     return args.n, None, v
 
@@ -176,7 +176,7 @@ def _cmd_bench(args) -> int:
                     r = _run(args.algo, n, None, v, args)
                     best = min(best, time.perf_counter() - t0)
                     cnt = len(r)
-                except ResourceLimitError as exc:
+                except errors.ResourceLimitError as exc:
                     err = str(exc)
                     break
             rep = {"engine": args.algo, "n": n, "density": d, "seed": args.seed,
@@ -241,10 +241,10 @@ def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
         return args.func(args)
-    except ResourceLimitError as exc:
+    except errors.ResourceLimitError as exc:
         sys.stderr.write(f"error: {exc}\n")
         return 2
-    except (ParseError, ValueError, OSError) as exc:
+    except (errors.ParseError, ValueError, OSError) as exc:
         sys.stderr.write(f"error: {exc}\n")
         return 1
 

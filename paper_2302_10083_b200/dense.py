@@ -22,7 +22,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .errors import ResourceLimitError
+from . import errors
 from .ternary import TruthTable, unrank_many
 
 MERGE = "merge"
@@ -67,7 +67,7 @@ def _cap_arg(n: int, hh: int, mem_cap: int | None) -> int:
     if cap <= 0:
         h = hh or min(n, DEFAULT_SPLIT)
         need = state_bytes(n, h)
-        raise ResourceLimitError(
+        raise errors.ResourceLimitError(
             f"dense state needs {need} bytes ({3 ** (n - h)} blocks of "
             f"{block_bits_for(h)} bits), exceeding the cap of {cap} bytes"
         )

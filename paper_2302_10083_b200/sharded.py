@@ -1,124 +1,275 @@
-"""Top-k-variable sharding of the dense path over 2^k ranks.
+"""Top-k-variable sharding of the dense path over 2^k GPUs.
 
-Rank g owns the binary assignment of the top k variables (bit j of g =
-variable n-k+1+j) and the contiguous truth-table slice [g*2^(n-k), (g+1)*2^(n-k)).
-With n' = n-k, the 3^k "top blocks" t in {0,1,*}^k each cover the contiguous
-rank range [rho(t)*3^n', (rho(t)+1)*3^n') and hold 3^n' cells in the h=5
-layout, so the global prime list is the concatenation of the blocks' lists in
-rho order. The algorithm (composition verified on the reference, SURVEY.md
-App. B.3):
+GPU g owns the assignment of the top k variables given by the bits of g, and
+its truth-table slice [g*2^(n-k), (g+1)*2^(n-k)) (the top variables are the
+most significant index bits). The 3^n cells are cut into SUPER-BLOCKS by the
+top K = k + m variables: super-block d is a K-digit ternary tuple (digits
+0..m-1 = variables n-K+1..n-k, the top of a GPU's own cube; digits m..K-1 =
+the k GPU variables), and it holds the 3^L cells (L = n - K) of the contiguous
+global rank range [rho(d)*3^L, (rho(d)+1)*3^L) in the h=5 layout. So the global
+prime list is the concatenation of the super-blocks' lists in rho order.
 
-1. local MERGE of the n' low dimensions on every binary block -> M_t;
-2. star blocks, one round per top axis j: M_t = M_{t[j->0]} AND M_{t[j->1]}
-   for the blocks whose highest star is j (block-level AND of dense.py:174-212);
-3. kills: K_t = OR over the fixed top digits j of M_{t[j->*]} (pre-reduce M,
-   as the oracle formula oracle.py:77-80 requires);
-4. P_t = REDUCE_low(M_t) AND NOT K_t, compacted to ranks + rho(t)*3^n'.
+Ownership (the interleaved rule of SURVEY.md §8(e), refined by super-block):
+bit j of owner(d) is the GPU digit t_j when it is 0/1, and bit j of
+h(s) = rho(s) mod 2^k when t_j is a star, s = the m local top digits. Then
+  * every binary-t super-block (t = bits of g) lies on g: the whole 3^(n-k)
+    cube of g is local and contiguous (slots 0..3^m-1 of g's arena);
+  * a star super-block's two children along its highest star GPU axis j
+    differ from it only in bit j of the owner: one is local, the other is on
+    peer g XOR e_j;
+  * each GPU holds ~1.5^k of the 3^k top blocks, i.e. 3^n/2^k cells:
+    125.5 GB of the 1.004 TB state at n=27 on 8 GPUs (127.6 GB with the
+    rounding of 3^m super-blocks; ShardPlan.budget).
+The algorithm (composition verified on the reference):
+  1. MERGE: each GPU merges its own cube (dqmc_merge_device); star
+     super-blocks are then, level by level (number of star GPU digits), the
+     AND of their two children, one read in place from the peer over NVLink
+     (block-level MERGE of dense.py:174-212, merge_triple dense.py:46-48).
+  2. REDUCE: super-block d's primes are REDUCE_low(M_d) AND NOT OR_i M_{d[i->*]}
+     over its fixed top digits i (oracle formula oracle.py:77-80; the parents
+     must be pre-REDUCE). The final pass reads the <= K parent super-blocks in
+     place (local or peer pointers) and applies the OR in registers: no kill
+     buffers, no staging copies. Levels run by the number of stars of d,
+     ascending, with a fence between levels: a super-block's readers (its
+     children) all belong to the level before its own, so it can be reduced
+     in place once that level is done.
+  3. Compaction per super-block, with its global rank offset.
+NCCL has no bitwise-AND reduction (nccl.h ops: sum/prod/max/min/avg) and the
+exchange here is pure peer loads, so the only collectives are the level
+fences and the one-time exchange of arena IPC handles.
 
-Blocks are placed by a deterministic greedy balance (every rank computes the
-same map); each block computed at its owner, inputs exchanged point-to-point.
-NCCL has no bitwise-AND reduction (nccl.h ops: sum/prod/max/min/avg), so the
-exchange is send/recv of whole blocks and the AND/OR runs in our kernels.
-
-The same schedule runs over a real process group, or over all 2^k ranks inside
-one process (``EmulatedComm``), which lets one GPU check k-GPU bit-exactness.
-Transports for a process group:
-  ``DistComm``  torch.distributed send/recv of whole blocks (NCCL on GPUs;
-                gloo with host staging for CPU tests and GPU-sharing tests);
-  ``IpcComm``   P2P: no transfer at all. Each rank exports CUDA IPC handles of
-                the blocks peers need; the peer opens them and our AND / OR
-                kernels read the owner's memory directly over NVLink (the
-                survey's fused peer-load design). Host-side
-                all_gather / barrier order the rounds; no kernel ever waits
-                on another process.
-Local compute is an ``ops`` object: ``GpuOps`` (libdqmc.so) in production;
-tests may pass a CPU implementation to exercise the host logic under gloo.
+The same schedule runs over all 2^k ranks inside one process
+(``EmulatedComm``: one GPU checks k-GPU bit-exactness) or one process per rank
+(``ProcessComm``: torch.distributed for the fences, arena handles exchanged
+once). Local compute is an ``ops`` object: ``GpuOps`` (libdqmc.so) in
+production; the CPU tests plug in oracle-backed ops over shared memory.
 """
 
 from __future__ import annotations
 
 import itertools
-from collections.abc import Iterable
+import json
+from dataclasses import dataclass
 
 import numpy as np
 
+MAX_KILL = 8  # parent super-blocks the final pass can read (kMaxKill, csrc/dqmc_internal.cuh)
+BALANCE = 1.02  # target max/ideal arena bytes when choosing m
+
+
+def rho(d) -> int:
+    """Rank of a digit tuple (digit i has weight 3^i)."""
+    return sum(int(x) * 3**i for i, x in enumerate(d))
+
+
+def state_bytes5(n: int) -> int:
+    """dqmc_state_bytes(n, 5): 3^(n-5) blocks of 256 bits (dense.py:56-63)."""
+    return 3 ** (n - 5) * 32
+
+
+def _owner(d, m: int, k: int) -> int:
+    hs = rho(d[:m]) % (1 << k) if k else 0
+    g = 0
+    for j in range(k):
+        t = d[m + j]
+        g |= (t if t < 2 else (hs >> j) & 1) << j
+    return g
+
+
+def _arena_counts(k: int, m: int) -> list[int]:
+    cnt = [0] * (1 << k)
+    for d in itertools.product((0, 1, 2), repeat=k + m):
+        cnt[_owner(d, m, k)] += 1
+    return cnt
+
+
+def choose_m(n: int, k: int) -> int:
+    """Smallest m whose super-block rounding keeps every GPU within BALANCE of
+    the ideal 3^n / 2^k cells, subject to K = k + m <= MAX_KILL and L >= 5."""
+    hi = min(MAX_KILL - k, n - k - 5)
+    if k == 0 or hi <= 0:
+        return 0
+    for m in range(1, hi + 1):
+        if max(_arena_counts(k, m)) * 2**k <= BALANCE * 3 ** (k + m):
+            return m
+    return hi
+
+
+@dataclass(frozen=True)
+class Ref:
+    """A super-block's location: rank and byte offset inside its arena."""
+
+    rank: int
+    off: int
+
+
+class ShardPlan:
+    """The whole schedule of one sharded call, identical on every rank."""
+
+    def __init__(self, n: int, k: int, m: int | None = None):
+        if not 0 <= k <= 3:
+            raise ValueError(f"k must be in 0..3 (1..8 GPUs), got {k}")
+        if n - k < 5:
+            raise ValueError(f"sharding needs n - k >= 5, got n={n}, k={k}")
+        self.n, self.k = n, k
+        self.m = choose_m(n, k) if m is None else int(m)
+        self.K = k + self.m
+        self.L = n - self.K
+        if self.m < 0 or self.K > MAX_KILL or self.L < 5:
+            raise ValueError(f"bad super-block split m={self.m} for n={n}, k={k}")
+        self.world = 1 << k
+        self.sb_bytes = state_bytes5(self.L)
+        m = self.m
+        self.blocks = sorted(itertools.product((0, 1, 2), repeat=self.K), key=rho)
+        self.owner = {d: _owner(d, m, k) for d in self.blocks}
+        # arena slots: the rank's own cube first (binary GPU digits = bits of g,
+        # local digits in rho order: exactly dqmc_merge_device's output), then
+        # its star super-blocks in rho order
+        self.slot: dict[tuple, int] = {}
+        nslots = [3**m] * self.world
+        for d in self.blocks:
+            t = d[m:]
+            if 2 not in t:
+                self.slot[d] = rho(d[:m])
+        for d in self.blocks:
+            if d not in self.slot:
+                g = self.owner[d]
+                self.slot[d] = nslots[g]
+                nslots[g] += 1
+        self.nslots = nslots
+        self.merge_levels = self._merge_levels()
+        self.reduce_levels = self._reduce_levels()
+
+    # -- layout
+    def ref(self, d) -> Ref:
+        return Ref(self.owner[d], self.slot[d] * self.sb_bytes)
+
+    def offset(self, d) -> int:
+        """Global rank of the super-block's first cell."""
+        return rho(d) * 3**self.L
+
+    def arena_bytes(self, g: int) -> int:
+        return self.nslots[g] * self.sb_bytes
+
+    # -- schedule
+    def _merge_levels(self):
+        """Level w (1..k): (d, child0, child1) for every super-block with w star
+        GPU digits, split along its highest star GPU digit."""
+        m = self.m
+        levels = []
+        for w in range(1, self.k + 1):
+            jobs = []
+            for d in self.blocks:
+                stars = [j for j in range(self.k) if d[m + j] == 2]
+                if len(stars) != w:
+                    continue
+                j = m + max(stars)
+                c0 = d[:j] + (0,) + d[j + 1 :]
+                c1 = d[:j] + (1,) + d[j + 1 :]
+                jobs.append((d, c0, c1))
+            levels.append(jobs)
+        return levels
+
+    def _reduce_levels(self):
+        """Level l (0..K): (d, parents) for every super-block with l stars; the
+        parents d[i->*] over its fixed digits are read pre-REDUCE (level l+1)."""
+        levels = [[] for _ in range(self.K + 1)]
+        for d in self.blocks:
+            parents = [d[:i] + (2,) + d[i + 1 :] for i in range(self.K) if d[i] != 2]
+            levels[sum(x == 2 for x in d)].append((d, parents))
+        return levels
+
+    # -- budget
+    def tile_bytes(self) -> int:
+        """Engine tile arrays of one super-block's final pass (20 B per C0 tile)."""
+        t = max(0, self.L - 5 - 7)
+        return 3**t * 20
+
+    def peak_device_bytes(self, g: int, rank_bytes: int = 0) -> int:
+        """Per-rank device peak: the arena, the rank's table slice (2^(n-k)
+        uint8) and its packed words, the engine's tile arrays, and the rank
+        output (0 when counting only)."""
+        nl = self.n - self.k
+        return self.arena_bytes(g) + (1 << nl) + (1 << nl) // 8 + self.tile_bytes() + rank_bytes
+
+    def budget(self) -> dict:
+        """Dry-run summary (bench.py --dry-run)."""
+        total = state_bytes5(self.n)
+        peaks = [self.peak_device_bytes(g) for g in range(self.world)]
+        recv = self.peer_read_bytes()
+        return {
+            "n": self.n, "k": self.k, "m": self.m, "gpus": self.world, "low_vars": self.L,
+            "super_blocks": len(self.blocks), "super_block_bytes": self.sb_bytes,
+            "state_bytes_total": total, "ideal_bytes_per_gpu": total // self.world,
+            "arena_bytes": [self.arena_bytes(g) for g in range(self.world)],
+            "peak_device_bytes": peaks, "max_peak_device_bytes": max(peaks),
+            "balance": max(peaks) / (total / self.world),
+            "merge_levels": len(self.merge_levels), "reduce_levels": len(self.reduce_levels),
+            "peer_read_bytes": recv,
+        }
+
+    def check_budget(self, g: int, free_bytes: int, rank_bytes: int = 0) -> int:
+        """Refuse before allocating, as load() does (dense.py:358-364): raise
+        ResourceLimitError naming the bytes rank g needs if they exceed
+        free_bytes. Returns the need."""
+        need = self.peak_device_bytes(g, rank_bytes)
+        if need > free_bytes:
+            from . import errors
+
+            raise errors.ResourceLimitError(
+                f"sharded n={self.n} on {self.world} GPUs: rank {g} needs {need} bytes "
+                f"({self.nslots[g]} super-blocks of {self.sb_bytes} bytes), only {free_bytes} bytes are free"
+            )
+        return need
+
+    def peer_read_bytes(self) -> list[int]:
+        """Bytes each rank reads from peers over the schedule (AND inputs + kills)."""
+        out = [0] * self.world
+        for jobs in self.merge_levels:
+            for d, c0, c1 in jobs:
+                g = self.owner[d]
+                out[g] += sum(self.sb_bytes for c in (c0, c1) if self.owner[c] != g)
+        for jobs in self.reduce_levels:
+            for d, parents in jobs:
+                g = self.owner[d]
+                out[g] += sum(self.sb_bytes for p in parents if self.owner[p] != g)
+        return out
+
 
 # ---------------------------------------------------------------------------
-# schedule (pure host logic)
+# the schedule
 
 
-def rho(t: tuple[int, ...]) -> int:
-    """Rank of a top-digit tuple (digit j has weight 3^j)."""
-    return sum(d * 3**j for j, d in enumerate(t))
+def run_schedule(plan: ShardPlan, inputs: dict, ops, comm, count_only: bool = False) -> dict:
+    """Run the sharded call. ``inputs[g]`` is rank g's table slice for every
+    rank local to ``comm``. Returns {d: result of ops.reduce_extract} for the
+    super-blocks those ranks own."""
+    local = comm.local_ranks()
+    for g in local:
+        ops.ensure_arena(g, plan.arena_bytes(g))
+    comm.share(ops)
+    nl = plan.n - plan.k
+    for g in local:
+        ops.merge(inputs[g], nl, Ref(g, 0))
+    comm.fence(ops)
+    for jobs in plan.merge_levels:
+        for d, c0, c1 in jobs:
+            if plan.owner[d] in local:
+                ops.and_(plan.ref(d), plan.ref(c0), plan.ref(c1), plan.sb_bytes)
+        comm.fence(ops)
+    out = {}
+    for jobs in plan.reduce_levels:
+        for d, parents in jobs:
+            if plan.owner[d] in local:
+                out[d] = ops.reduce_extract(plan.ref(d), plan.L, [plan.ref(p) for p in parents], plan.offset(d),
+                                            count_only)
+        comm.fence(ops)
+    return out
 
 
-def all_blocks(k: int) -> list[tuple[int, ...]]:
-    """Every top block, in rho (= global rank) order."""
-    return sorted(itertools.product((0, 1, 2), repeat=k), key=rho)
-
-
-def binary_block(g: int, k: int) -> tuple[int, ...]:
-    return tuple((g >> j) & 1 for j in range(k))
-
-
-def owner_map(k: int) -> dict[tuple[int, ...], int]:
-    """Deterministic balanced placement: each block goes to the least loaded
-    rank whose bits agree with the block's fixed digits (binary blocks to
-    their own rank)."""
-    load = [0] * (1 << k)
-    own: dict[tuple[int, ...], int] = {}
-    for t in sorted(all_blocks(k), key=lambda t: (sum(d == 2 for d in t), rho(t))):
-        cands = [g for g in range(1 << k) if all(((g >> j) & 1) == d for j, d in enumerate(t) if d != 2)]
-        best = min(cands, key=lambda g: (load[g], g))
-        own[t] = best
-        load[best] += 1
-    return own
-
-
-def highest_star(t: tuple[int, ...]) -> int:
-    stars = [j for j, d in enumerate(t) if d == 2]
-    return max(stars) if stars else -1
-
-
-def children(t: tuple[int, ...], j: int) -> tuple[tuple[int, ...], tuple[int, ...]]:
-    return tuple(0 if i == j else d for i, d in enumerate(t)), tuple(1 if i == j else d for i, d in enumerate(t))
-
-
-def parents(t: tuple[int, ...]) -> list[tuple[int, ...]]:
-    return [tuple(2 if i == j else d for i, d in enumerate(t)) for j, d in enumerate(t) if d != 2]
-
-
-def star_rounds(k: int) -> list[list[tuple[tuple, tuple, tuple]]]:
-    """Round j: (t, c0, c1) for every block whose highest star axis is j."""
-    rounds = []
-    for j in range(k):
-        jobs = []
-        for t in all_blocks(k):
-            if highest_star(t) == j:
-                c0, c1 = children(t, j)
-                jobs.append((t, c0, c1))
-        rounds.append(jobs)
-    return rounds
-
-
-def transfer_volume(k: int) -> dict[int, int]:
-    """Blocks each rank receives over the whole schedule (for DESIGN notes / tests)."""
-    own = owner_map(k)
-    recv = {g: 0 for g in range(1 << k)}
-    for jobs in star_rounds(k):
-        seen = set()
-        for t, c0, c1 in jobs:
-            for c in (c0, c1):
-                if own[c] != own[t] and (c, own[t]) not in seen:
-                    seen.add((c, own[t]))
-                    recv[own[t]] += 1
-    seen = set()
-    for t in all_blocks(k):
-        for p in parents(t):
-            if own[p] != own[t] and (p, own[t]) not in seen:
-                seen.add((p, own[t]))
-                recv[own[t]] += 1
-    return recv
+def ordered(parts: dict) -> list:
+    """Results in global rank order (super-blocks are disjoint rank ranges)."""
+    return [parts[d] for d in sorted(parts, key=rho)]
 
 
 # ---------------------------------------------------------------------------
@@ -126,7 +277,7 @@ def transfer_volume(k: int) -> dict[int, int]:
 
 
 class EmulatedComm:
-    """All 2^k ranks inside one process: a transfer is a reference."""
+    """All 2^k ranks inside one process: every arena is local."""
 
     def __init__(self, world: int):
         self.world = world
@@ -134,209 +285,58 @@ class EmulatedComm:
     def local_ranks(self) -> list[int]:
         return list(range(self.world))
 
-    def is_local(self, r: int) -> bool:
-        return True
-
-    def exchange(self, transfers, held, ops):
-        return {(dst, c): held[(src, c)] for c, src, dst in transfers}
-
-    def done_reading(self, ops):
+    def share(self, ops):
         pass
 
-    def barrier(self):
+    def fence(self, ops):
+        ops.sync()
+
+    def close(self, ops):
         pass
 
 
-class DistComm:
-    """One rank of a torch.distributed process group (NCCL or gloo).
+class ProcessComm:
+    """One rank per process of a torch.distributed group (NCCL on 8 GPUs;
+    gloo for CPU tests and for several ranks sharing one GPU). ``share``
+    exchanges each arena's handle once (CUDA IPC on GPUs, a shared-memory name
+    on CPU); every later access is a peer load inside our kernels. ``fence``
+    = local stream sync + barrier: no kernel ever waits on another process."""
 
-    staging=True moves device blocks through host memory (gloo cannot send
-    CUDA tensors); it lets several processes share one GPU in tests, since no
-    kernel ever waits on another process — only the host-side exchange does."""
-
-    def __init__(self, group=None, staging: bool = False):
+    def __init__(self, group=None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
-        self.staging = staging
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._shared = None
 
     def local_ranks(self) -> list[int]:
         return [self.rank]
 
-    def is_local(self, r: int) -> bool:
-        return r == self.rank
+    def share(self, ops):
+        key = ops.arena_key(self.rank)
+        if self._shared == key:
+            return  # arenas unchanged since the last call: handles still open
+        if self._shared is not None:
+            ops.close_peers()
+        mine = ops.export_arena(self.rank)
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        for g, h in enumerate(allh):
+            if g != self.rank:
+                ops.import_arena(g, h)
+        self._shared = key
 
-    def exchange(self, transfers, held, ops):
-        """Point-to-point block moves, posted in the same global order on
-        every rank so sends and receives pair up deterministically."""
-        dist = self.dist
-        ops.sync()  # blocks about to be sent must be complete
-        reqs, out, staged = [], {}, []
-        for c, src, dst in transfers:
-            if src == self.rank:
-                t = held[(src, c)]
-                if self.staging and t.is_cuda:
-                    t = t.cpu()
-                    staged.append(t)
-                reqs.append(dist.isend(t, dst, group=self.group))
-            elif dst == self.rank:
-                buf = ops.empty_block()
-                if self.staging and buf.is_cuda:
-                    host = buf.new_empty(buf.shape, device="cpu")
-                    reqs.append(dist.irecv(host, src, group=self.group))
-                    staged.append((buf, host))
-                else:
-                    reqs.append(dist.irecv(buf, src, group=self.group))
-                out[(dst, c)] = buf
-        for r in reqs:
-            r.wait()
-        for x in staged:
-            if isinstance(x, tuple):
-                x[0].copy_(x[1])
-        ops.sync()
-        return out
-
-    def done_reading(self, ops):
-        pass  # received blocks are private copies
-
-    def barrier(self):
-        self.dist.barrier(group=self.group)
-
-
-class PeerBlock:
-    """A block that lives in a peer process's device memory (opened via CUDA
-    IPC): duck-types the two tensor methods the block ops use."""
-
-    def __init__(self, ptr: int, numel: int):
-        self._ptr, self._numel = ptr, numel
-
-    def data_ptr(self) -> int:
-        return self._ptr
-
-    def numel(self) -> int:
-        return self._numel
-
-
-class IpcComm(DistComm):
-    """P2P transport over CUDA IPC (see the module docstring). Round protocol:
-    every rank finishes its stream, then all-gathers (block, owner, handle,
-    offset) for the blocks others need; consumers open each peer allocation
-    once and read it in place. ``done_reading`` (sync + barrier) fences the
-    owners' in-place REDUCE behind the peers' last reads."""
-
-    def __init__(self, group=None):
-        super().__init__(group, staging=False)
-        from . import _lib
-
-        self._lib = _lib
-        self._opened: dict = {}  # (owner rank, owner base address) -> local base pointer
-
-    def exchange(self, transfers, held, ops):
-        import ctypes
-
-        L = self._lib.load()
-        ops.sync()  # blocks peers will read are complete before anyone reads them
-        mine = []
-        for c, src, dst in transfers:
-            if src == self.rank:
-                t = held[(src, c)]
-                h = ctypes.create_string_buffer(64)
-                off = ctypes.c_uint64(0)
-                self._lib.check(L.dqmc_ipc_get(t.data_ptr(), h, ctypes.byref(off)))
-                mine.append((c, dst, h.raw, int(off.value), t.data_ptr() - int(off.value), int(t.numel())))
-        allx = [None] * self.world
-        self.dist.all_gather_object(allx, mine, group=self.group)
-        out = {}
-        for src, lst in enumerate(allx):
-            for c, dst, hb, off, base_id, numel in lst:
-                if dst != self.rank:
-                    continue
-                key = (src, base_id)
-                if key not in self._opened:
-                    p = ctypes.c_void_p()
-                    self._lib.check(L.dqmc_ipc_open(hb, ctypes.byref(p)))
-                    self._opened[key] = int(p.value)
-                out[(dst, c)] = PeerBlock(self._opened[key] + off, numel)
-        return out
-
-    def done_reading(self, ops):
+    def fence(self, ops):
         ops.sync()
         self.dist.barrier(group=self.group)
-        L = self._lib.load()
-        for base in self._opened.values():
-            self._lib.check(L.dqmc_ipc_close(base))
-        self._opened.clear()
 
-
-def _dedupe(transfers: Iterable[tuple]) -> list[tuple]:
-    seen, out = set(), []
-    for x in transfers:
-        if x not in seen:
-            seen.add(x)
-            out.append(x)
-    return out
-
-
-# ---------------------------------------------------------------------------
-# the sharded algorithm
-
-
-def sharded_prime_ranks(inputs: dict, n: int, k: int, ops, comm) -> dict:
-    """Run the schedule. ``inputs[g]`` is rank g's local table slice (for the
-    ranks local to ``comm``). Returns {top block t: ranks of P_t (global
-    ranks, ascending)} for the blocks owned by local ranks."""
-    nl = n - k
-    if nl < 5:
-        raise ValueError(f"sharding needs n - k >= 5, got n={n}, k={k}")
-    own = owner_map(k)
-    held: dict = {}
-    for g in comm.local_ranks():
-        held[(g, binary_block(g, k))] = ops.merge(inputs[g], nl)
-    # (2) star blocks, one round per top axis
-    for jobs in star_rounds(k):
-        transfers = _dedupe((c, own[c], own[t]) for t, c0, c1 in jobs for c in (c0, c1) if own[c] != own[t])
-        recv = comm.exchange(transfers, held, ops)
-        for t, c0, c1 in jobs:
-            o = own[t]
-            if comm.is_local(o):
-                a = held[(o, c0)] if (o, c0) in held else recv[(o, c0)]
-                b = held[(o, c1)] if (o, c1) in held else recv[(o, c1)]
-                held[(o, t)] = ops.and_(a, b)
-        del recv
-    # received children were temporaries; keep only owned blocks
-    held = {(g, t): v for (g, t), v in held.items() if own[t] == g}
-    # (3) kills from the top-axis parents (pre-reduce M)
-    transfers = _dedupe((p, own[p], own[t]) for t in all_blocks(k) for p in parents(t) if own[p] != own[t])
-    recv = comm.exchange(transfers, held, ops)
-    kills = {}
-    for t in all_blocks(k):
-        o = own[t]
-        if not comm.is_local(o):
-            continue
-        kill = None
-        for p in parents(t):
-            src = held[(o, p)] if (o, p) in held else recv[(o, p)]
-            kill = ops.copy(src) if kill is None else ops.or_(kill, src)
-        kills[t] = kill
-    del recv
-    ops.sync()
-    comm.done_reading(ops)  # P2P: peers have read every M_t before it is reduced in place
-    # (4) reduce the low dimensions, apply the kills, compact with the block offset
-    out = {}
-    for t in all_blocks(k):
-        o = own[t]
-        if comm.is_local(o):
-            out[t] = ops.reduce_extract(held[(o, t)], nl, kills[t], rho(t) * 3**nl)
-    return out
-
-
-def concat_ranks(parts: dict) -> np.ndarray:
-    """Global ascending rank list from {t: ranks} (blocks are disjoint rank ranges)."""
-    arrs = [np.asarray(parts[t]) for t in sorted(parts, key=rho)]
-    return np.concatenate(arrs).astype(np.int64) if arrs else np.zeros(0, dtype=np.int64)
+    def close(self, ops):
+        if self._shared is not None:
+            self.fence(ops)
+            ops.close_peers()
+            self._shared = None
 
 
 # ---------------------------------------------------------------------------
@@ -344,90 +344,138 @@ def concat_ranks(parts: dict) -> np.ndarray:
 
 
 class GpuOps:
-    """Local compute on the current CUDA device through the C ABI."""
+    """Super-block compute on the current CUDA device through the C ABI.
+    Ranks of every super-block are written back to back into one device
+    buffer (``out``); reduce_extract returns the (start, count) span."""
 
-    def __init__(self, n_local: int, device=None):
+    def __init__(self, device=None):
         import torch
 
         from . import _lib
-        from .dense import state_bytes
 
         self.torch = torch
         self._lib = _lib
         self.L = _lib.load()
-        self.nl = n_local
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.words = state_bytes(n_local, 5) // 4
-        self.rank_buf = None
+        self.arenas: dict[int, object] = {}  # local rank -> uint8 tensor
+        self.bases: dict[int, int] = {}  # rank -> device address of its arena (local or IPC-mapped)
+        self._opened: list[int] = []
+        self.out = None
+        self.cursor = 0
 
     def _stream(self):
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
-    def empty_block(self):
-        return self.torch.empty(self.words, dtype=self.torch.int32, device=self.device)
+    def ptr(self, ref: Ref) -> int:
+        return self.bases[ref.rank] + ref.off
 
     def sync(self):
         self.torch.cuda.current_stream(self.device).synchronize()
 
-    def merge(self, values, nl):
-        out = self.empty_block()
-        kind = self._lib.IN_U8 if values.dtype == self.torch.uint8 else self._lib.IN_WORDS
-        self._lib.check(self.L.dqmc_merge_device(values.data_ptr(), kind, nl, out.data_ptr(), self._stream()))
-        return out
+    def ensure_arena(self, g: int, nbytes: int):
+        a = self.arenas.get(g)
+        if a is None or a.numel() < nbytes:
+            self.arenas[g] = None
+            a = self.torch.empty(max(nbytes, 16), dtype=self.torch.uint8, device=self.device)
+            self.arenas[g] = a
+        self.bases[g] = a.data_ptr()
 
-    def _bitop(self, a, b, op, out=None):
-        out = self.empty_block() if out is None else out
-        self._lib.check(self.L.dqmc_bitop_device(out.data_ptr(), a.data_ptr(), b.data_ptr(), a.numel() * 4, op,
-                                                 self._stream()))
-        return out
+    def arena_key(self, g: int):
+        return self.arenas[g].data_ptr()
 
-    def and_(self, a, b):
-        return self._bitop(a, b, 0)
-
-    def or_(self, dst, src):
-        return self._bitop(dst, src, 1, out=dst)
-
-    def copy(self, src):
-        if isinstance(src, self.torch.Tensor):
-            return src.clone()
-        return self._bitop(src, src, 0)  # a peer block: x & x, read over P2P
-
-    def reduce_extract(self, block, nl, kill, offset):
+    def export_arena(self, g: int):
         import ctypes
 
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64(0)
+        self._lib.check(self.L.dqmc_ipc_get(self.arenas[g].data_ptr(), h, ctypes.byref(off)))
+        return (h.raw, int(off.value))
+
+    def import_arena(self, g: int, handle):
+        import ctypes
+
+        raw, off = handle
+        p = ctypes.c_void_p()
+        self._lib.check(self.L.dqmc_ipc_open(raw, ctypes.byref(p)))
+        self._opened.append(int(p.value))
+        self.bases[g] = int(p.value) + off
+
+    def close_peers(self):
+        for base in self._opened:
+            self._lib.check(self.L.dqmc_ipc_close(base))
+        self._opened.clear()
+
+    def reset_output(self):
+        self.cursor = 0
+
+    def merge(self, values, nl: int, dst: Ref):
+        kind = self._lib.IN_U8 if values.dtype == self.torch.uint8 else self._lib.IN_WORDS
+        self._lib.check(self.L.dqmc_merge_device(values.data_ptr(), kind, nl, self.ptr(dst), self._stream()))
+
+    def and_(self, dst: Ref, a: Ref, b: Ref, nbytes: int):
+        self._lib.check(self.L.dqmc_bitop_device(self.ptr(dst), self.ptr(a), self.ptr(b), nbytes, 0, self._stream()))
+
+    def reduce_extract(self, ref: Ref, L: int, kills: list, offset: int, count_only: bool):
+        import ctypes
+
+        kp = (ctypes.c_void_p * max(1, len(kills)))(*[self.ptr(r) for r in kills])
         cnt = ctypes.c_int64(0)
-        if self.rank_buf is None:
-            self.rank_buf = self.torch.empty(1 << 22, dtype=self.torch.int64, device=self.device)
-        kp = kill.data_ptr() if kill is not None else None
-        work = block  # reduced in place (all readers of M_t are done)
+        flags = self._lib.FLAG_COUNT_ONLY if count_only else 0
+        if count_only:
+            self._lib.check(self.L.dqmc_reduce_extract_device(self.ptr(ref), L, kp, len(kills), int(offset), None, 0,
+                                                              ctypes.byref(cnt), flags, self._stream()))
+            return int(cnt.value)
+        if self.out is None:
+            self.out = self.torch.empty(1 << 22, dtype=self.torch.int64, device=self.device)
         for _ in range(2):
-            self._lib.check(self.L.dqmc_reduce_extract_device(
-                work.data_ptr(), nl, kp, int(offset), self.rank_buf.data_ptr(), self.rank_buf.numel(),
-                ctypes.byref(cnt), 0, self._stream()))
-            if cnt.value <= self.rank_buf.numel():
+            free = self.out.numel() - self.cursor
+            dst = self.out.data_ptr() + 8 * self.cursor
+            self._lib.check(self.L.dqmc_reduce_extract_device(self.ptr(ref), L, kp, len(kills), int(offset), dst,
+                                                              free, ctypes.byref(cnt), flags, self._stream()))
+            c = int(cnt.value)
+            if c <= free:
                 break
-            # REDUCE is idempotent and the kills are applied outside the block,
-            # so the already-reduced block can simply be extracted again
-            self.rank_buf = self.torch.empty(int(cnt.value * 1.1) + 1024, dtype=self.torch.int64, device=self.device)
-        return self.rank_buf[: cnt.value].clone()
+            # grow the output and extract again: REDUCE is idempotent and the
+            # kills are read, never written, so the reduced block is reusable
+            bigger = self.torch.empty(max(2 * self.out.numel(), self.cursor + int(c * 1.25) + 1024),
+                                      dtype=self.torch.int64, device=self.device)
+            bigger[: self.cursor].copy_(self.out[: self.cursor])
+            self.out = bigger
+        span = (self.cursor, c)
+        self.cursor += c
+        return span
+
+    def gather(self, parts: dict):
+        """Device int64 ranks of the given super-blocks in global rank order."""
+        spans = ordered(parts)
+        if not spans:
+            return self.torch.zeros(0, dtype=self.torch.int64, device=self.device)
+        return self.torch.cat([self.out[s : s + c] for s, c in spans])
 
 
-def gpu_sharded_prime_ranks_emulated(values_full, n: int, k: int) -> np.ndarray:
-    """All 2^k shards on the current GPU, one after another (no collective):
-    the k-GPU schedule, checked bit-exact against the 1-GPU engine."""
-    import torch
-
+def gpu_sharded_prime_ranks_emulated(values_full, n: int, k: int, m: int | None = None) -> np.ndarray:
+    """All 2^k ranks on the current GPU in one process (no collective): the
+    k-GPU schedule, checked bit-exact against the 1-GPU engine."""
+    plan = ShardPlan(n, k, m)
     nl = n - k
-    ops = GpuOps(nl)
-    inputs = {g: values_full[g << nl : (g + 1) << nl] for g in range(1 << k)}
-    parts = sharded_prime_ranks(inputs, n, k, ops, EmulatedComm(1 << k))
-    return concat_ranks({t: v.cpu().numpy() for t, v in parts.items()})
+    ops = GpuOps()
+    inputs = {g: values_full[g << nl : (g + 1) << nl] for g in range(plan.world)}
+    parts = run_schedule(plan, inputs, ops, EmulatedComm(plan.world))
+    return ops.gather(parts).cpu().numpy()
+
+
+def dry_run(n: int, k: int) -> dict:
+    return ShardPlan(n, k).budget()
+
+
+# ---------------------------------------------------------------------------
+# bench.py under torchrun (N > 1)
 
 
 def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
-    """bench.py under torchrun (N > 1): config-4 workload sharded on the top
-    log2(N) variables; device time of the whole schedule, max over ranks."""
-    import json
+    """The workload sharded on the top log2(N) variables, one rank per GPU;
+    CUDA-event time of the whole schedule, max over ranks. The same n at every
+    N (total work fixed): strong scaling."""
     import os
 
     import torch
@@ -441,79 +489,96 @@ def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
     backend = os.environ.get("DQMC_DIST_BACKEND", "nccl")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
-    else:  # gloo with host staging (tests: several ranks sharing one GPU)
+    else:  # gloo (several ranks sharing one GPU in tests)
         dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     k = world.bit_length() - 1
     if 1 << k != world:
         raise SystemExit("world size must be a power of two")
     n = args.n
+    plan = ShardPlan(n, k)
     nl = n - k
-    # this rank's slice of the frozen generator: points [rank*2^nl, (rank+1)*2^nl)
+    count_only = n > 25  # config 5: 3-4e10 primes (~300 GB of ranks); the deliverable is counts
+    free, _ = torch.cuda.mem_get_info()
+    plan.check_budget(rank, free)
     vals = torch.empty(1 << nl, dtype=torch.uint8, device="cuda")
     _lib.check(_lib.load().dqmc_gen3_range_device(vals.data_ptr(), rank << nl, 1 << nl, workload["p_on"],
                                                    workload["p_dc"], workload["seed"],
                                                    torch.cuda.current_stream().cuda_stream))
-    ops = GpuOps(nl)
-    # DQMC_DIST_TRANSPORT=p2p: CUDA-IPC peer reads (IpcComm); default: block send/recv
-    if os.environ.get("DQMC_DIST_TRANSPORT", "sendrecv") == "p2p":
-        comm = IpcComm()
-    else:
-        comm = DistComm(staging=backend != "nccl")
+    ops = GpuOps()
+    comm = ProcessComm()
 
-    def step():
-        parts = sharded_prime_ranks({rank: vals}, n, k, ops, comm)
-        return sum(int(v.numel()) for v in parts.values())
+    def step(src):
+        ops.reset_output()
+        parts = run_schedule(plan, {rank: src}, ops, comm, count_only=count_only)
+        return parts
 
-    # e2e step: this rank's slice from pinned host memory, its primes back to the host
+    def primes_of(parts):
+        return sum(int(v) if count_only else int(v[1]) for v in parts.values())
+
     host_vals = torch.empty(1 << nl, dtype=torch.uint8, pin_memory=True)
     host_vals.copy_(vals.cpu())
     h2d = torch.empty_like(vals)
 
-    def e2e_step():
-        h2d.copy_(host_vals, non_blocking=True)
-        parts = sharded_prime_ranks({rank: h2d}, n, k, ops, comm)
-        outs = [v.cpu() for v in parts.values()]
-        return sum(int(o.numel()) for o in outs)
-
     for _ in range(args.warmup):
-        step()
+        step(vals)
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    cnt = 0
+    parts = None
     for _ in range(args.steps):
-        cnt = step()
+        parts = step(vals)
     e1.record()
     torch.cuda.synchronize()
-    # e2e (host buffers) under the same barrier + max-over-ranks rule
+    cnt = primes_of(parts)
+    # e2e: this rank's slice from pinned host memory, its primes back to the host
     dist.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
+    d2h = 0
     for _ in range(args.steps):
-        e2e_step()
+        h2d.copy_(host_vals, non_blocking=True)
+        parts = step(h2d)
+        if count_only:
+            d2h = 8 * len(parts)
+        else:
+            host = ops.gather(parts).cpu()
+            d2h = host.numel() * 8
     e3.record()
     torch.cuda.synchronize()
     dev = "cuda" if backend == "nccl" else "cpu"
     t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps, e2.elapsed_time(e3) / 1e3 / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    c = torch.tensor([cnt], device=dev, dtype=torch.int64)
+    c = torch.tensor([cnt, d2h], device=dev, dtype=torch.int64)
     dist.all_reduce(c)
+    comm.close(ops)
     if rank == 0:
         tmax = float(t[0].item())
         te2e = float(t[1].item())
+        b = plan.budget()
         line = {
             "metric": metric, "value": 3**n / tmax, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tmax * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (frozen generator, per-rank slice on device)",
-            "config": {"workload": "BASELINE config 4 sharded on the top log2(N) variables", "n": n, "k": k,
-                       "primes": int(c.item()), "backend": backend},
+            "config": {"workload": workload.get("name", "sharded"), "n": n, "k": k, "m": plan.m,
+                       "primes": int(c[0].item()), "count_only": count_only, "backend": backend,
+                       "max_peak_device_bytes": b["max_peak_device_bytes"]},
             "e2e": {"value": 3**n / te2e, "unit": unit, "ms_per_step": te2e * 1e3,
-                    "h2d_bytes_per_step": int(1 << n), "d2h_bytes_per_step": int(c.item()) * 8},
+                    "h2d_bytes_per_step": int(1 << n), "d2h_bytes_per_step": int(c[1].item())},
             "gpu_launches": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+if __name__ == "__main__":  # pragma: no cover
+    import argparse
+
+    ap = argparse.ArgumentParser(description="per-rank byte budget of the sharded plan (no GPU needed)")
+    ap.add_argument("--n", type=int, default=27)
+    ap.add_argument("--k", type=int, default=3)
+    a = ap.parse_args()
+    print(json.dumps(dry_run(a.n, a.k), indent=1))

@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .dense import DEFAULT_SPLIT, MERGE, REDUCE, block_bits_for, state_bytes
-from .errors import ResourceLimitError
+from . import errors
 from .ternary import unrank_many
 
 _OPS = {MERGE: 0, REDUCE: 1}
@@ -150,7 +150,7 @@ def load(tt, h: int | None = None, mem_cap: int | None = None, optimized: bool =
         raise ValueError(f"split must be in 1..{n}, got {h}")
     need = state_bytes(n, h)
     if mem_cap is not None and need > mem_cap:
-        raise ResourceLimitError(
+        raise errors.ResourceLimitError(
             f"dense state needs {need} bytes ({3 ** (n - h)} blocks of "
             f"{block_bits_for(h)} bits), exceeding the cap of {mem_cap} bytes"
         )

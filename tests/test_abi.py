@@ -121,3 +121,13 @@ def test_count_primes_cap_validated_like_load(pkg):
     for cap in (0, -5):
         with pytest.raises(pkg.ResourceLimitError, match=str(pkg.state_bytes(12, 5))):
             pkg.count_primes(tt, mem_cap=cap)
+
+
+def test_sparse_cap_validated_before_the_device(pkg):
+    # sparse.py:105-111: an explicit cap <= 0 cannot hold the level-0 table
+    tt = pkg.TruthTable.full(10)
+    with pytest.raises(pkg.ResourceLimitError, match="sparse level table needs 16384 bytes"):
+        pkg.sparse_prime_ranks(tt, mem_cap=0)
+    assert pkg.ENGINES == ("dense", "sparse")
+    with pytest.raises(ValueError, match="oracle"):
+        pkg.run_engine("oracle", tt)

@@ -1,14 +1,17 @@
-"""Top-k sharding: schedule logic, gloo multi-process runs on
-CPU (world_size 2 and 4, 127.0.0.1), and the k-shard schedule on one GPU
-compared bit-exactly with the single-GPU engine.
+"""Top-k sharding: the super-block plan and its byte budget,
+the schedule on CPU (one process, and gloo worlds of 2 and 4 processes whose
+arenas live in shared memory, the CPU stand-in for CUDA IPC), and on the GPU
+the k-rank schedule compared bit-exactly with the single-GPU engine.
 
-On CPU the per-block compute is done by the oracle (test infrastructure); the
-code under test is the schedule + point-to-point exchange in
+On CPU the per-super-block compute is done by the oracle (test
+infrastructure); the code under test is the plan + schedule in
 paper_2302_10083_b200.sharded, which is the same code the GPU path runs.
 """
 
+import hashlib
 import os
 import socket
+from multiprocessing import shared_memory
 
 import numpy as np
 import pytest
@@ -19,84 +22,188 @@ import torch.multiprocessing as mp
 from paper_2302_10083_b200 import sharded as S
 
 
-class OracleOps:
-    """CPU block ops for tests: oracle MERGE / REDUCE on h=5 blocks."""
+class CpuOps:
+    """Oracle MERGE / REDUCE over numpy arenas in POSIX shared memory: a peer
+    arena is opened by name exactly as a GPU peer arena is opened by its IPC
+    handle, and read in place."""
 
-    def __init__(self, nl):
+    def __init__(self):
         from oracle import oracle as O
 
         self.O = O
-        self.nl = nl
-        self.words = O.state_bytes(nl, 5) // 8
+        self.shm = {}  # rank -> SharedMemory (own and opened peers)
+        self.own = set()
 
-    def empty_block(self):
-        return torch.empty(self.words, dtype=torch.int64)
+    def ensure_arena(self, g, nbytes):
+        if g in self.shm and self.shm[g].size >= nbytes:
+            return
+        self.shm[g] = shared_memory.SharedMemory(create=True, size=max(nbytes, 16))
+        self.own.add(g)
+
+    def arena_key(self, g):
+        return self.shm[g].name
+
+    def export_arena(self, g):
+        return self.shm[g].name
+
+    def import_arena(self, g, name):
+        self.shm[g] = shared_memory.SharedMemory(name=name)
+
+    def close_peers(self):
+        for g in [g for g in self.shm if g not in self.own]:
+            self.shm.pop(g).close()
+
+    def release(self):
+        self.close_peers()
+        for g in list(self.own):
+            self.shm[g].close()
+            self.shm[g].unlink()
+        self.shm.clear()
+        self.own.clear()
 
     def sync(self):
         pass
 
-    def merge(self, values, nl):
+    def words(self, ref, nbytes):
+        return np.ndarray((nbytes // 8,), dtype=np.uint64, buffer=self.shm[ref.rank].buf, offset=ref.off)
+
+    def merge(self, values, nl, dst):
         from oracle import gen as G
 
         st = self.O.OracleState(G.values_to_words(values), nl, 5)
         st.run_pass(self.O.MERGE)
-        return torch.from_numpy(st.words.view(np.int64).copy())
+        self.words(dst, st.words.nbytes)[:] = st.words
 
-    def and_(self, a, b):
-        return torch.bitwise_and(a, b)
+    def and_(self, dst, a, b, nbytes):
+        np.bitwise_and(self.words(a, nbytes), self.words(b, nbytes), out=self.words(dst, nbytes))
 
-    def or_(self, dst, src):
-        return dst.bitwise_or_(src)
-
-    def copy(self, src):
-        return src.clone()
-
-    def reduce_extract(self, block, nl, kill, offset):
-        st = self.O.OracleState.from_words(block.numpy().view(np.uint64).copy(), nl, 5)
+    def reduce_extract(self, ref, L, kills, offset, count_only):
+        nb = self.O.state_bytes(L, 5)
+        w = self.words(ref, nb)
+        st = self.O.OracleState.from_words(w.copy(), L, 5)
         st.run_pass(self.O.REDUCE)
-        if kill is not None:
-            st.words &= ~kill.numpy().view(np.uint64)
-        return st.extract_ranks() + offset
+        w[:] = st.words  # reduced in place, as the GPU does
+        kill = np.zeros_like(st.words)
+        for p in kills:
+            kill |= self.words(p, nb)
+        st.words &= ~kill
+        r = st.extract_ranks() + offset
+        return len(r) if count_only else r
 
 
-class TestSchedule:
+# ---------------------------------------------------------------------------
+# the plan
+
+
+class TestPlan:
+    @pytest.mark.parametrize("n,k", [(12, 1), (13, 2), (14, 3), (24, 3), (27, 3), (24, 1)])
+    def test_ownership_rules(self, n, k):
+        p = S.ShardPlan(n, k)
+        m = p.m
+        assert p.K <= S.MAX_KILL and p.L >= 5
+        # every super-block has one owner; a rank's own cube is local, contiguous, in rho order
+        for d in p.blocks:
+            g = p.owner[d]
+            t = d[m:]
+            assert all(((g >> j) & 1) == x for j, x in enumerate(t) if x != 2)
+            if 2 not in t:
+                assert g == sum(x << j for j, x in enumerate(t)) and p.slot[d] == S.rho(d[:m])
+        # slots of a rank are distinct and dense
+        for g in range(p.world):
+            slots = sorted(p.slot[d] for d in p.blocks if p.owner[d] == g)
+            assert slots == list(range(p.nslots[g]))
+        assert sum(p.nslots) * p.sb_bytes == S.state_bytes5(n)
+
     @pytest.mark.parametrize("k", [1, 2, 3])
-    def test_owner_map(self, k):
-        own = S.owner_map(k)
-        assert len(own) == 3**k
-        for g in range(1 << k):
-            assert own[S.binary_block(g, k)] == g
-        for t, g in own.items():  # owner agrees with every fixed digit
-            assert all(((g >> j) & 1) == d for j, d in enumerate(t) if d != 2)
-        loads = np.bincount(list(own.values()), minlength=1 << k)
-        assert loads.max() - loads.min() <= 1  # balanced to within one block
+    def test_merge_children_local_or_one_peer(self, k):
+        p = S.ShardPlan(17, k)
+        done = {d for d in p.blocks if 2 not in d[p.m:]}
+        for jobs in p.merge_levels:
+            for d, c0, c1 in jobs:
+                assert c0 in done and c1 in done  # children computed in an earlier level
+                g = p.owner[d]
+                owners = {p.owner[c0], p.owner[c1]}
+                assert g in owners
+                other = (owners - {g}) or {g}
+                assert bin(other.pop() ^ g).count("1") <= 1  # the other child is on g XOR e_j
+            done |= {d for d, _, _ in jobs}
+        assert done == set(p.blocks)
 
     @pytest.mark.parametrize("k", [1, 2, 3])
-    def test_rounds_cover_every_star_block_once(self, k):
-        seen = [t for jobs in S.star_rounds(k) for t, _, _ in jobs]
-        stars = [t for t in S.all_blocks(k) if 2 in t]
-        assert sorted(seen) == sorted(stars)
-        done = {t for t in S.all_blocks(k) if 2 not in t}
-        for jobs in S.star_rounds(k):  # children always computed in an earlier round
-            for t, c0, c1 in jobs:
-                assert c0 in done and c1 in done
-            done |= {t for t, _, _ in jobs}
+    def test_reduce_parents_are_read_before_they_are_reduced(self, k):
+        p = S.ShardPlan(16, k)
+        level = {d: lvl for lvl, jobs in enumerate(p.reduce_levels) for d, _ in jobs}
+        assert set(level) == set(p.blocks)
+        for lvl, jobs in enumerate(p.reduce_levels):
+            for d, parents in jobs:
+                assert len(parents) <= S.MAX_KILL
+                assert all(level[q] == lvl + 1 for q in parents)
 
-    def test_block_ranges_tile_the_rank_space(self):
-        k, nl = 2, 6
-        ranges = sorted((S.rho(t) * 3**nl, (S.rho(t) + 1) * 3**nl) for t in S.all_blocks(k))
-        assert ranges[0][0] == 0 and ranges[-1][1] == 3 ** (nl + k)
+    def test_super_blocks_tile_the_rank_space(self):
+        p = S.ShardPlan(12, 2)
+        ranges = sorted((p.offset(d), p.offset(d) + 3**p.L) for d in p.blocks)
+        assert ranges[0][0] == 0 and ranges[-1][1] == 3**12
         assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
 
-    @pytest.mark.parametrize("n,k", [(8, 1), (9, 2), (10, 3), (11, 2)])
-    def test_emulated_cpu_matches_single_engine(self, n, k, oracle_mod, gen_mod):
-        v = gen_mod.gen3(n, 0.7, 0.1, n)
-        nl = n - k
-        inputs = {g: v[g << nl : (g + 1) << nl] for g in range(1 << k)}
-        parts = S.sharded_prime_ranks(inputs, n, k, OracleOps(nl), S.EmulatedComm(1 << k))
-        got = S.concat_ranks({t: x for t, x in parts.items()})
-        want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
-        assert np.array_equal(got, want)
+    def test_config5_fits_eight_b200(self):
+        """n=27 on 8 GPUs: every rank's peak (arena + table slice + words +
+        tile arrays) stays under 150 GB of a B200's ~180 GB."""
+        b = S.ShardPlan(27, 3).budget()
+        assert b["max_peak_device_bytes"] <= 150e9
+        assert b["balance"] <= 1.02
+        assert sum(b["arena_bytes"]) == 3**22 * 32  # state_bytes(27, 5) = 1.004 TB in total
+
+    @pytest.mark.parametrize("k", [1, 2, 3])
+    def test_n24_arena_is_one_over_2k_of_the_state(self, k):
+        p = S.ShardPlan(24, k)
+        ideal = S.state_bytes5(24) / 2**k
+        assert max(p.arena_bytes(g) for g in range(p.world)) <= 1.03 * ideal
+
+    def test_over_budget_raises_before_allocating(self, pkg):
+        p = S.ShardPlan(27, 3)
+        need = p.peak_device_bytes(0)
+        assert p.check_budget(0, need) == need
+        with pytest.raises(pkg.ResourceLimitError, match=str(need)):
+            p.check_budget(0, need - 1)
+
+    def test_bad_splits(self):
+        with pytest.raises(ValueError):
+            S.ShardPlan(8, 4)
+        with pytest.raises(ValueError):
+            S.ShardPlan(7, 3)
+        with pytest.raises(ValueError):
+            S.ShardPlan(20, 3, m=6)  # K = 9 > MAX_KILL
+
+    def test_dry_run_cli(self):
+        import json
+        import subprocess
+        import sys
+
+        r = subprocess.run([sys.executable, "-m", "paper_2302_10083_b200.sharded", "--n", "27", "--k", "3"],
+                           capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stderr
+        b = json.loads(r.stdout)
+        assert b["gpus"] == 8 and b["max_peak_device_bytes"] <= 150e9
+
+
+# ---------------------------------------------------------------------------
+# the schedule on CPU
+
+
+@pytest.mark.parametrize("n,k,m", [(8, 1, None), (9, 2, None), (10, 3, None), (11, 2, 2), (12, 3, 3), (11, 1, 0)])
+def test_emulated_cpu_matches_single_engine(n, k, m, oracle_mod, gen_mod):
+    v = gen_mod.gen3(n, 0.7, 0.1, n)
+    plan = S.ShardPlan(n, k, m)
+    nl = n - k
+    ops = CpuOps()
+    try:
+        inputs = {g: v[g << nl : (g + 1) << nl] for g in range(plan.world)}
+        parts = S.run_schedule(plan, inputs, ops, S.EmulatedComm(plan.world))
+        got = np.concatenate(S.ordered(parts)).astype(np.int64)
+    finally:
+        ops.release()
+    want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
+    assert np.array_equal(got, want)
 
 
 def _free_port():
@@ -109,22 +216,28 @@ def _worker(rank, world, port, n, seed, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    ops = CpuOps()
     try:
         from oracle import gen as G
 
         k = world.bit_length() - 1
+        plan = S.ShardPlan(n, k)
         nl = n - k
         v = G.gen3(n, 0.75, 0.05, seed)
-        mine = v[rank << nl : (rank + 1) << nl]
-        parts = S.sharded_prime_ranks({rank: mine}, n, k, OracleOps(nl), S.DistComm())
+        comm = S.ProcessComm()
+        parts = S.run_schedule(plan, {rank: v[rank << nl : (rank + 1) << nl]}, ops, comm)
+        comm.close(ops)
         gathered = [None] * world if rank == 0 else None
-        dist.gather_object({t: np.asarray(x) for t, x in parts.items()}, gathered, dst=0)
+        dist.gather_object(parts, gathered, dst=0)
         if rank == 0:
             allp = {}
             for d in gathered:
                 allp.update(d)
-            np.save(os.path.join(outdir, "ranks.npy"), S.concat_ranks(allp))
+            assert set(allp) == set(plan.blocks)
+            np.save(os.path.join(outdir, "ranks.npy"), np.concatenate(S.ordered(allp)).astype(np.int64))
+        dist.barrier()
     finally:
+        ops.release()
         dist.destroy_process_group()
 
 
@@ -137,49 +250,55 @@ def test_gloo_sharded_equals_single(world, n, tmp_path, oracle_mod, gen_mod):
     assert np.array_equal(got, want)
 
 
+# ---------------------------------------------------------------------------
+# the schedule on the GPU
+
+
+def _block_diff(got, want, plan):
+    out = [f"total got {len(got)} want {len(want)}"]
+    for d in plan.blocks:
+        lo, hi = plan.offset(d), plan.offset(d) + 3**plan.L
+        g, w = got[(got >= lo) & (got < hi)], want[(want >= lo) & (want < hi)]
+        if not np.array_equal(g, w):
+            out.append(f"super-block {d} (owner {plan.owner[d]}): got {len(g)} want {len(w)}")
+    return "; ".join(out[:12])
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,k", [(12, 1), (14, 2), (17, 3), (20, 2), (22, 3)])
-def test_gpu_emulated_shards_bit_exact(n, k, pkg, gen_mod):
+@pytest.mark.parametrize("n,k", [(12, 1), (14, 2), (17, 3), (20, 2), (22, 3), (21, 1)])
+def test_gpu_emulated_shards_bit_exact(n, k, pkg):
     from paper_2302_10083_b200 import device
 
     vd = device.gen3_device(n, 0.75, 0.05, 3)
     got = S.gpu_sharded_prime_ranks_emulated(vd, n, k)
     want = pkg.prime_ranks_from_values(vd.cpu().numpy())
-    assert np.array_equal(got, want), _block_diff(got, want, n, k)
-
-
-def _block_diff(got, want, n, k):
-    nl = n - k
-    out = [f"total got {len(got)} want {len(want)}"]
-    for t in S.all_blocks(k):
-        lo, hi = S.rho(t) * 3**nl, (S.rho(t) + 1) * 3**nl
-        g, w = got[(got >= lo) & (got < hi)], want[(want >= lo) & (want < hi)]
-        if not np.array_equal(g, w):
-            out.append(f"block {t}: got {len(g)} want {len(w)} missing {len(np.setdiff1d(w, g))} extra {len(np.setdiff1d(g, w))}")
-    return "; ".join(out)
+    assert np.array_equal(got, want), _block_diff(got, want, S.ShardPlan(n, k))
 
 
 @pytest.mark.gpu
 @pytest.mark.slow
-def test_gpu_emulated_config4_k3(pkg, golden):
-    """n=24 on 8 emulated shards == the reference's pins for config 4."""
-    import hashlib
-
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_gpu_emulated_config4(k, pkg, golden):
+    """n=24 on 2^k emulated ranks == the reference's pins for config 4."""
     from paper_2302_10083_b200 import device
 
     g = golden["configs"]["4"]
     vd = device.gen3_device(24, 0.75, 0.05, 3)
-    got = S.gpu_sharded_prime_ranks_emulated(vd, 24, 3)
+    got = S.gpu_sharded_prime_ranks_emulated(vd, 24, k)
+    del vd
     if len(got) != g["primes"]:
-        want = pkg.prime_ranks_from_values(vd.cpu().numpy())
-        raise AssertionError(_block_diff(got, want, 24, 3))
+        from paper_2302_10083_b200 import device as D
+
+        want = pkg.prime_ranks_from_values(D.gen3_device(24, 0.75, 0.05, 3).cpu().numpy())
+        raise AssertionError(_block_diff(got, want, S.ShardPlan(24, k)))
     assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()[:16] == g["ranks_sha256_prefix"]
+    torch.cuda.empty_cache()
 
 
-def _gpu_worker(rank, world, port, n, outdir, transport="staging"):
-    """One rank of a multi-process run sharing cuda:0: real GPU block ops; the
-    exchange is host-staged gloo send/recv, or P2P reads of the peers' blocks
-    through CUDA IPC (no kernel waits on another process either way)."""
+def _gpu_worker(rank, world, port, n, outdir):
+    """One rank of a multi-process run sharing cuda:0: real GPU kernels, peer
+    arenas opened through CUDA IPC and read in place (no kernel waits on
+    another process; the level fences are host barriers)."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -188,49 +307,53 @@ def _gpu_worker(rank, world, port, n, outdir, transport="staging"):
         from paper_2302_10083_b200 import _lib
 
         k = world.bit_length() - 1
+        plan = S.ShardPlan(n, k)
         nl = n - k
         vals = torch.empty(1 << nl, dtype=torch.uint8, device="cuda")
         _lib.check(_lib.load().dqmc_gen3_range_device(vals.data_ptr(), rank << nl, 1 << nl, 0.75, 0.05, 3,
                                                        torch.cuda.current_stream().cuda_stream))
-        comm = S.IpcComm() if transport == "p2p" else S.DistComm(staging=True)
-        parts = S.sharded_prime_ranks({rank: vals}, n, k, S.GpuOps(nl), comm)
+        ops = S.GpuOps()
+        comm = S.ProcessComm()
+        for _ in range(2):  # the second call reuses the arenas and the open peer handles
+            ops.reset_output()
+            parts = S.run_schedule(plan, {rank: vals}, ops, comm)
+        mine = {d: ops.out[s : s + c].cpu().numpy() for d, (s, c) in parts.items()}
+        comm.close(ops)
         gathered = [None] * world if rank == 0 else None
-        dist.gather_object({t: v.cpu().numpy() for t, v in parts.items()}, gathered, dst=0)
+        dist.gather_object(mine, gathered, dst=0)
         if rank == 0:
             allp = {}
             for d in gathered:
                 allp.update(d)
-            np.save(os.path.join(outdir, "ranks.npy"), S.concat_ranks(allp))
+            np.save(os.path.join(outdir, "ranks.npy"), np.concatenate(S.ordered(allp)).astype(np.int64))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["staging", "p2p"])
 @pytest.mark.parametrize("world,n", [(2, 18), (4, 19)])
-def test_gpu_multiprocess_sharded(world, n, transport, tmp_path, pkg):
+def test_gpu_multiprocess_sharded(world, n, tmp_path, pkg):
     """The sharded data path with GpuOps on real kernels, ranks as processes,
-    over both transports (send/recv with host staging; CUDA-IPC peer reads)."""
+    peer super-blocks read through CUDA IPC."""
     from paper_2302_10083_b200 import device
 
-    mp.spawn(_gpu_worker, args=(world, _free_port(), n, str(tmp_path), transport), nprocs=world, join=True)
+    mp.spawn(_gpu_worker, args=(world, _free_port(), n, str(tmp_path)), nprocs=world, join=True)
     got = np.load(tmp_path / "ranks.npy")
     want = pkg.prime_ranks_from_values(device.gen3_device(n, 0.75, 0.05, 3).cpu().numpy())
-    assert np.array_equal(got, want), _block_diff(got, want, n, world.bit_length() - 1)
+    assert np.array_equal(got, want), _block_diff(got, want, S.ShardPlan(n, world.bit_length() - 1))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["sendrecv", "p2p"])
-def test_bench_torchrun_two_ranks_gloo(transport, tmp_path, pkg):
+def test_bench_torchrun_two_ranks_gloo(tmp_path, pkg):
     """bench.py under torch.distributed.run (N=2) through the sharded path, gloo
-    backend (host-staged send/recv, or CUDA-IPC peer reads) so both ranks can
-    share this run's single GPU."""
+    backend so both ranks can share this run's single GPU (peer reads over
+    CUDA IPC)."""
     import json
     import subprocess
     import sys
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DQMC_DIST_BACKEND="gloo", DQMC_DIST_TRANSPORT=transport)
+    env = dict(os.environ, DQMC_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1", "--nvars", "18"]
