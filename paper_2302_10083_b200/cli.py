@@ -6,10 +6,12 @@ Mirrors the dense-path subset of the reference CLI
   primes  all prime implicants of one function, one string per line,
           wildcard count descending then rank ascending (cli.py:131-138);
           the ordering runs on the GPU (dqmc_order_by_weight)
-  verify  run two independent GPU engines on the same input and compare
+  verify  run independent GPU engines on the same input and compare
           (cli.py:141-177): "dense" = the fused multi-pass plan
-          (dense_prime_ranks), "state" = the per-dimension device DenseState
-          (the reference's layer structure, csrc/dqmc_state.cu)
+          (dense_prime_ranks), "sparse" = the level walk over device hash
+          sets (sparse_prime_ranks, csrc/dqmc_sparse.cu), "state" = the
+          per-dimension device DenseState (the reference's layer structure,
+          csrc/dqmc_state.cu)
   bench   timed runs over sweeps of generated inputs, JSONL reports with the
           reference's BenchReport fields (bench.py:38-56)
 
@@ -37,11 +39,12 @@ import numpy as np
 
 from . import _lib
 from .dense import dense_prime_ranks, prime_ranks_from_values
+from .sparse import sparse_prime_ranks
 from . import errors
 from .ternary import TruthTable, ranks_to_text
 
 _CORRUPT_ENV = "IMPLICANTS_VERIFY_CORRUPT"  # same fault-injection hook as cli.py:40-42
-ENGINES = ("dense", "state")
+ENGINES = ("dense", "sparse", "state")
 
 
 class _Parser(argparse.ArgumentParser):
@@ -110,6 +113,10 @@ def _run(engine: str, n: int, tt, values, args) -> np.ndarray:
         if tt is not None:
             return dense_prime_ranks(tt, h=args.h, optimized=args.unroll == "on", mem_cap=args.mem_cap)
         return prime_ranks_from_values(values, h=args.h, mem_cap=args.mem_cap)
+    if engine == "sparse":
+        if tt is None:
+            tt = TruthTable.from_values(n, values)
+        return sparse_prime_ranks(tt, mem_cap=args.mem_cap)
     if engine == "state":
         if tt is None:
             tt = TruthTable.from_values(n, values)
@@ -220,7 +227,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.set_defaults(func=_cmd_primes)
     p = sub.add_parser("verify", help="compare engines on one input")
     _add_common(p)
-    p.add_argument("--algo", default="dense,state", help="comma list of engines")
+    p.add_argument("--algo", default="dense,sparse", help="comma list of engines (dense, sparse, state)")
     p.set_defaults(func=_cmd_verify)
     p = sub.add_parser("bench", help="time the engine over generated inputs (JSONL)")
     p.add_argument("--n", dest="n_sweep", required=True, help="e.g. 16..22 or 20,24")

@@ -82,9 +82,30 @@ __device__ inline uint64_t shl_w(const uint64_t *v, int64_t k, int64_t s) {
 }
 
 // In-block dimension i (d = 3^(i-1)) on every block; masks = (3, wpb) digit
-// masks of dim i (dense.py:70-88). Each thread owns one block and works in a
-// private scratch copy (wpb words in global scratch) so shifted reads see the
-// original block.
+// masks of dim i (dense.py:70-88). Blocks of up to 4 words (h <= 5, every
+// split the engine and the reference's defaults use) are copied to registers
+// first (k_state_bottom_dim_reg), so shifted reads see the original block;
+// wider blocks (h >= 6) work in a private scratch copy in global memory.
+template <int W>
+__global__ void k_state_bottom_dim_reg(uint64_t *__restrict__ w, int64_t blocks, int64_t d,
+                                       const uint64_t *__restrict__ masks, int op) {
+    const int64_t stride = gridDim.x * (int64_t)blockDim.x;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < blocks; a += stride) {
+        uint64_t *v = w + a * W;
+        uint64_t o[W];
+#pragma unroll
+        for (int k = 0; k < W; k++) o[k] = v[k];
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+            if (op == 0) {
+                v[k] = o[k] | (shl_w(o, k, 2 * d) & shl_w(o, k, d) & masks[2 * W + k]);
+            } else {
+                v[k] = o[k] & ~((shr_w(o, W, k, 2 * d) & masks[k]) | (shr_w(o, W, k, d) & masks[W + k]));
+            }
+        }
+    }
+}
+
 __global__ void k_state_bottom_dim(uint64_t *__restrict__ w, uint64_t *__restrict__ tmp, int64_t blocks, int64_t wpb,
                                    int64_t d, const uint64_t *__restrict__ masks, int op) {
     const int64_t stride = gridDim.x * (int64_t)blockDim.x;
@@ -196,11 +217,16 @@ int dqmc_state_create(int n, int h, uint64_t mem_cap, dqmc_state_t **out) {
     st->used = p3(h);
     st->blocks = blocks;
     st->nw = blocks * st->wpb;
-    if (cudaMalloc(&st->words, (size_t)st->nw * 8) != cudaSuccess || cudaMalloc(&st->tmp, (size_t)st->nw * 8) != cudaSuccess ||
+    // blocks wider than 4 words (h >= 6) need a scratch copy for the in-block dims
+    const bool scratch = st->wpb > 4;
+    st->tmp = nullptr;
+    if (cudaMalloc(&st->words, (size_t)st->nw * 8) != cudaSuccess ||
+        (scratch && cudaMalloc(&st->tmp, (size_t)st->nw * 8) != cudaSuccess) ||
         cudaMalloc(&st->masks, (size_t)3 * h * st->wpb * 8) != cudaSuccess) {
         (void)cudaGetLastError();
         dqmc_state_free(st);
-        return fail(DQMC_ERR_RESOURCE, "device allocation of " + std::to_string(need * 2) + " bytes failed");
+        return fail(DQMC_ERR_RESOURCE,
+                    "device allocation of " + std::to_string(need * (scratch ? 2 : 1)) + " bytes failed");
     }
     // digit masks (dense.py:70-88): masks[(i-1)][d][k]
     std::vector<uint64_t> m((size_t)3 * h * st->wpb, 0);
@@ -274,8 +300,16 @@ int dqmc_state_run_pass(dqmc_state_t *st, int op, const int *dims, int ndims, in
             k_state_top_dim<<<grid_for(groups * inner), 256>>>(st->words, groups, inner, op);
             if (counts) counts[k] = groups * inner / st->wpb;
         } else {
-            k_state_bottom_dim<<<grid_for(st->blocks), 256>>>(st->words, st->tmp, st->blocks, st->wpb, p3(dim - 1),
-                                                              st->masks + (size_t)(dim - 1) * 3 * st->wpb, op);
+            const uint64_t *mk = st->masks + (size_t)(dim - 1) * 3 * st->wpb;
+            if (st->wpb == 1)
+                k_state_bottom_dim_reg<1><<<grid_for(st->blocks), 256>>>(st->words, st->blocks, p3(dim - 1), mk, op);
+            else if (st->wpb == 2)
+                k_state_bottom_dim_reg<2><<<grid_for(st->blocks), 256>>>(st->words, st->blocks, p3(dim - 1), mk, op);
+            else if (st->wpb == 4)
+                k_state_bottom_dim_reg<4><<<grid_for(st->blocks), 256>>>(st->words, st->blocks, p3(dim - 1), mk, op);
+            else
+                k_state_bottom_dim<<<grid_for(st->blocks), 256>>>(st->words, st->tmp, st->blocks, st->wpb, p3(dim - 1),
+                                                                  mk, op);
             if (counts) counts[k] = -1;
         }
         SCK(cudaGetLastError());

@@ -48,8 +48,8 @@ class TestGpu:
 
     def test_engines_byte_identical(self, capsys):
         base = ["--n", "12", "--density", "0.5", "--seed", "6"]
-        outs = {a: run(["primes", "--algo", a, *base], capsys)[1] for a in ("dense", "state")}
-        assert outs["dense"] == outs["state"] and len(outs["dense"]) > 0
+        outs = {a: run(["primes", "--algo", a, *base], capsys)[1] for a in ("dense", "sparse", "state")}
+        assert outs["dense"] == outs["state"] == outs["sparse"] and len(outs["dense"]) > 0
 
     def test_order_matches_numpy_lexsort(self, pkg, gen_mod):
         from paper_2302_10083_b200.cli import order_for_listing
@@ -61,7 +61,9 @@ class TestGpu:
     def test_verify_ok_and_mismatch(self, capsys, monkeypatch):
         code, out, _ = run(["verify", "--n", "11", "--density", "0.6", "--dc", "0.1"], capsys)
         assert code == 0 and out.startswith("OK")
-        monkeypatch.setenv("IMPLICANTS_VERIFY_CORRUPT", "state")
+        code, out, _ = run(["verify", "--algo", "dense,sparse,state", "--n", "12", "--density", "0.3"], capsys)
+        assert code == 0 and "dense, sparse, state" in out
+        monkeypatch.setenv("IMPLICANTS_VERIFY_CORRUPT", "sparse")
         code, _, err = run(["verify", "--n", "11", "--density", "0.6"], capsys)
         assert code == 3 and "MISMATCH" in err
 

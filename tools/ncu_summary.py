@@ -36,12 +36,10 @@ def short(name: str) -> str:
     tmpl = m.group(2) or ""
     if base == "k_merge_reduce_pipe":
         return "k_strided<MERGE_REDUCE>"
-    if base == "k_strided_pipe":
-        mode = tmpl.strip("<>").split(",")[-1].strip()
-        return {"1": "k_strided<MERGE_REDUCE>", "2": "k_strided<REDUCE>"}.get(mode, base + tmpl)
-    if base == "k_strided":
-        mode = tmpl.strip("<>").split(",")[-1].strip()
-        return {"0": "k_strided<MERGE_ONLY>"}.get(mode, base + tmpl)
+    if base == "k_strided_pipe":  # pass D (reduce-only since round 2)
+        return "k_strided<REDUCE>"
+    if base == "k_strided":  # pass B (merge-only since round 2)
+        return "k_strided<MERGE_ONLY>"
     return base
 
 
@@ -81,12 +79,13 @@ def main():
             f"{vals.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
             f"{vals.get('smsp__inst_executed.sum', 0):.3g} | {vals.get('launch__registers_per_thread', 0):.0f} |"
         )
-    with open(os.path.join(os.path.dirname(md) or ".", "ncu_summary.json"), "w") as fh:
-        json.dump(out, fh, indent=1)
+    if "--no-json" not in sys.argv:  # the table bench.py reads its roofline traffic from
+        with open(os.path.join(os.path.dirname(md) or ".", "ncu_summary.json"), "w") as fh:
+            json.dump(out, fh, indent=1)
     with open(md, "w") as fh:
         fh.write(f"# ncu --set full summary ({os.path.basename(rep)}, n={n})\n\n")
         fh.write("Captured with `ncu --set full --clock-control none --import-source on` on one B200 ")
-        fh.write("(`tools/run_once.py`), one launch per kernel; per-launch values (cold-cache, serialised).\n\n")
+        fh.write("(`tools/run_once.py` or `tools/run_sparse_once.py`), one launch per kernel; per-launch values (cold-cache, serialised).\n\n")
         fh.write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
