@@ -133,19 +133,20 @@ class TestContract:
 
 
 class TestPipelinedHostPath:
-    @pytest.mark.parametrize("n", [13, 17, 20])
-    def test_pipelined_equals_plain(self, pkg, oracle_mod, gen_mod, n, monkeypatch):
+    @pytest.mark.parametrize("n", [13, 17, 20, 23])
+    def test_pipelined_equals_plain(self, pkg, oracle_mod, gen_mod, n):
         """The host API pipelines the final stage (chunked, copied out over
-        PCIe while the next chunk computes) once it has a size hint."""
+        PCIe while the next chunk computes) once it has a size hint. n = 23
+        runs the piece-major plan (pass C's sparse stores + validity bitmap)."""
+        from paper_2302_10083_b200 import _lib
+
+        _lib.load().dqmc_release()  # no size hint: the first call takes the plain path
         v = gen_mod.gen3(n, 0.8, 0.05, 11)
         want = oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v), n)
-        first = pkg.prime_ranks_from_values(v)  # sets the hint
+        first = pkg.prime_ranks_from_values(v)  # plain; sets the hint
         second = pkg.prime_ranks_from_values(v)  # pipelined
-        monkeypatch.setenv("DQMC_NO_PIPELINE", "1")
-        plain = pkg.prime_ranks_from_values(v)
-        assert np.array_equal(first, want) and np.array_equal(second, want) and np.array_equal(plain, want)
+        assert np.array_equal(first, want) and np.array_equal(second, want)
         # a larger output than the hint (grow path): denser table, same n
-        monkeypatch.delenv("DQMC_NO_PIPELINE")
         v2 = gen_mod.gen3(n, 0.95, 0.0, 12)
         got = pkg.prime_ranks_from_values(v2)
         assert np.array_equal(got, oracle_mod.dense_prime_ranks(gen_mod.values_to_words(v2), n))
@@ -199,20 +200,31 @@ class TestFullSize:
         hr = pkg.prime_ranks_from_values(v.cpu().numpy())
         assert np.array_equal(hr, host)
 
-    def test_config4_n24_plan_variants(self, pkg, golden, monkeypatch):
-        """The opt-in plan variants (sparse pass D over C's nonzero-row bits;
-        the contiguous-tile layout without piece-major group 0) give the same
-        ranks as the default plan."""
-        from paper_2302_10083_b200 import device
+    def test_config4_n24_reference_layout_plan(self, pkg, golden):
+        """The bitmap-keeping plan (reference layout, no piece-major group 0,
+        no sparse pass-C stores) counts the same primes as the default plan,
+        and a default call after it (reusing the state buffer, whose stale
+        contents pass D must mask) is still exact."""
+        import ctypes
+
+        import torch
+
+        from paper_2302_10083_b200 import _lib, device
 
         g = golden["configs"]["4"]
         v = device.gen3_device(24, 0.75, 0.05, 3)
-        for env, val in (("DQMC_SPARSE_D", "1"), ("DQMC_SPARSE_D", "2"), ("DQMC_NO_PM", "1")):
-            monkeypatch.setenv(env, val)
-            r, cnt = device.dense_prime_ranks_device(v, 24)
-            monkeypatch.delenv(env)
-            assert cnt == g["primes"], env
-            assert rsha(r.cpu().numpy())[:16] == g["ranks_sha256_prefix"], env
+        cnt = ctypes.c_int64(0)
+        _lib.check(_lib.load().dqmc_primes_device(v.data_ptr(), _lib.IN_U8, 24, None, 0, ctypes.byref(cnt),
+                                                  _lib.FLAG_KEEP_BITMAP | _lib.FLAG_COUNT_ONLY,
+                                                  torch.cuda.current_stream().cuda_stream))
+        assert cnt.value == g["primes"]
+        r, c2 = device.dense_prime_ranks_device(v, 24)
+        assert c2 == g["primes"] and rsha(r.cpu().numpy())[:16] == g["ranks_sha256_prefix"]
+        # a different table in between leaves different stale rows behind
+        w = device.gen3_device(24, 0.5, 0.1, 9)
+        device.dense_prime_ranks_device(w, 24, count_only=True)
+        r, c3 = device.dense_prime_ranks_device(v, 24)
+        assert c3 == g["primes"] and rsha(r.cpu().numpy())[:16] == g["ranks_sha256_prefix"]
 
 
 @pytest.mark.slow
