@@ -291,8 +291,13 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
     if ((rc = engine_begin(s))) return rc;
     CK(cudaMemcpyAsync(g_eng.in_tmp, host_in, in_bytes, cudaMemcpyHostToDevice, s));
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0;
+    // the chunked final stage overlaps the rank D2H with the last chunks'
+    // compute; it pays one host round trip per chunk (16), so it only runs
+    // when the hinted output is large enough for the overlap to win (>= 4M
+    // ranks = 32 MB; config 2's 0.4M ranks: 0.79 -> ~0.3 ms per call)
+    constexpr int64_t kPipelineMinRanks = (int64_t)1 << 22;
     const bool pipelined = !count_only && !(flags & (DQMC_FLAG_KEEP_BITMAP | DQMC_FLAG_TIMING)) && p.T > 0 &&
-                           g_eng.hint_n == n && g_eng.hint_count > 0;
+                           g_eng.hint_n == n && g_eng.hint_count >= kPipelineMinRanks;
     if (pipelined) {
         // merge/reduce passes, then the chunked final stage straight into pinned host memory
         g_eng.state_n = -1;  // the state is overwritten in the plan's own layout

@@ -315,9 +315,13 @@ class ProcessComm:
         return [self.rank]
 
     def share(self, ops):
-        key = ops.arena_key(self.rank)
-        if self._shared == key:
-            return  # arenas unchanged since the last call: handles still open
+        # every rank learns every arena's identity; if none changed since the
+        # last call the opened peer handles are still valid (one small
+        # all-gather per call), else all ranks re-export and re-open
+        keys = [None] * self.world
+        self.dist.all_gather_object(keys, ops.arena_key(self.rank), group=self.group)
+        if self._shared == keys:
+            return
         if self._shared is not None:
             ops.close_peers()
         mine = ops.export_arena(self.rank)
@@ -326,7 +330,7 @@ class ProcessComm:
         for g, h in enumerate(allh):
             if g != self.rank:
                 ops.import_arena(g, h)
-        self._shared = key
+        self._shared = keys
 
     def fence(self, ops):
         ops.sync()

@@ -136,8 +136,9 @@ class TestPipelinedHostPath:
     @pytest.mark.parametrize("n", [13, 17, 20, 23])
     def test_pipelined_equals_plain(self, pkg, oracle_mod, gen_mod, n):
         """The host API pipelines the final stage (chunked, copied out over
-        PCIe while the next chunk computes) once it has a size hint. n = 23
-        runs the piece-major plan (pass C's sparse stores + validity bitmap)."""
+        PCIe while the next chunk computes) once it has a size hint of at
+        least 4M ranks (n = 20, 23 here; n = 13, 17 stay on the plain path).
+        n = 23 runs the piece-major plan."""
         from paper_2302_10083_b200 import _lib
 
         _lib.load().dqmc_release()  # no size hint: the first call takes the plain path
