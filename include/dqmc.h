@@ -46,7 +46,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DQMC_ABI_VERSION 2
+#define DQMC_ABI_VERSION 3
 
 /* status codes */
 #define DQMC_OK 0
@@ -178,22 +178,31 @@ int dqmc_gen_sbox_host(uint8_t *values_host, uint64_t seed); /* 2^20 bytes */
 int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_t *out_host);
 
 /* Building blocks of the sharded multi-GPU path (SURVEY.md §8(e),
- * DESIGN.md §6), all on device buffers in the h = 5 layout (n >= 5):
+ * DESIGN.md §6), all on device buffers in the h = 5 layout (n >= 5), all
+ * stream-ordered on `stream` (no host synchronisation unless stated):
  * dqmc_merge_device: complete MERGE of all n dimensions (no REDUCE) into
  *   state_out (dqmc_state_bytes(n, 5) bytes) — the implicant bitmap M of
  *   the (sub-)function, DenseState.words after run_pass(MERGE) (dense.py:296-315).
- * dqmc_reduce_extract_device: REDUCE of all n dimensions in place, then clear
- *   every cell set in any of the nkill (<= 8) bitmaps kills[] — the top-axis
- *   parent super-blocks, pre-reduce, read in place (local or peer memory) —
- *   then ordered compaction of the survivors as ranks + rank_offset. ranks_dev
- *   NULL or DQMC_FLAG_COUNT_ONLY: count only. If the count exceeds ranks_cap,
- *   *count_out is the true count and nothing beyond ranks_cap is written.
- * dqmc_bitop_device: dst = a & b (op 0) or a | b (op 1), nbytes % 16 == 0. */
+ * dqmc_bitop_device: dst = a & b (op 0) or a | b (op 1), nbytes % 16 == 0.
+ * dqmc_bitop_batch_device: the same for njobs (dst, a, b) address triples
+ *   stored in device memory (one launch per merge level; a/b may be peer memory).
+ * dqmc_reduce_low_device: REDUCE of all n dimensions of nslots consecutive
+ *   states (super-blocks) in place.
+ * dqmc_extract_kills_device: for nslots low-reduced states, clear in every
+ *   state the OR of its parent states (kill_tab: nslots x 8 device addresses,
+ *   null padded, local or peer memory) and compact the survivors as ranks +
+ *   rank_add[slot] into ranks_dev, slot after slot; slot_start / slot_count
+ *   (device) receive each slot's range and *total_out (host) the total. The
+ *   one call that synchronises the stream. ranks_dev NULL or
+ *   DQMC_FLAG_COUNT_ONLY: counts only. If the total exceeds ranks_cap, nothing
+ *   beyond ranks_cap is written and *total_out is the true total. */
 int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state_out, void *stream);
-int dqmc_reduce_extract_device(uint32_t *state, int n, const uint32_t *const *kills, int nkill, int64_t rank_offset,
-                               int64_t *ranks_dev, int64_t ranks_cap, int64_t *count_out, uint32_t flags,
-                               void *stream);
 int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint64_t nbytes, int op, void *stream);
+int dqmc_bitop_batch_device(const uint64_t *jobs_dev, int64_t njobs, uint64_t nbytes, int op, void *stream);
+int dqmc_reduce_low_device(uint32_t *arena, int n, int64_t nslots, void *stream);
+int dqmc_extract_kills_device(const uint32_t *arena, int n, int64_t nslots, const uint64_t *kill_tab,
+                              const int64_t *rank_add, int64_t *ranks_dev, int64_t ranks_cap, int64_t *slot_start,
+                              int64_t *slot_count, int64_t *total_out, uint32_t flags, void *stream);
 
 /* Peer access for the sharded path's P2P transport (one process per GPU):
  * a rank exports a CUDA IPC handle of the allocation holding its arena of

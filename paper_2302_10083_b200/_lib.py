@@ -62,7 +62,9 @@ EXPORTS = (
     "dqmc_ipc_close",
     "dqmc_order_by_weight",
     "dqmc_merge_device",
-    "dqmc_reduce_extract_device",
+    "dqmc_reduce_low_device",
+    "dqmc_extract_kills_device",
+    "dqmc_bitop_batch_device",
     "dqmc_bitop_device",
     "dqmc_plan",
     "dqmc_release",
@@ -160,8 +162,10 @@ def load() -> ctypes.CDLL:
             "dqmc_ipc_close": (i32, [vp]),
             "dqmc_order_by_weight": (i32, [vp, i64, i32, vp]),
             "dqmc_merge_device": (i32, [vp, i32, i32, vp, vp]),
-            "dqmc_reduce_extract_device": (i32, [vp, i32, vp, i32, i64, vp, i64, ctypes.POINTER(ctypes.c_int64), u32,
-                                                 vp]),
+            "dqmc_reduce_low_device": (i32, [vp, i32, i64, vp]),
+            "dqmc_extract_kills_device": (i32, [vp, i32, i64, vp, vp, vp, i64, vp, vp, ctypes.POINTER(ctypes.c_int64),
+                                                u32, vp]),
+            "dqmc_bitop_batch_device": (i32, [vp, i64, u64, i32, vp]),
             "dqmc_bitop_device": (i32, [vp, vp, vp, u64, i32, vp]),
             "dqmc_plan": (i32, [i32, ctypes.POINTER(ctypes.c_int64), i32]),
             "dqmc_release": (None, []),

@@ -68,7 +68,12 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
     uint32_t pk[kPk];
 #pragma unroll
     for (int i = 0; i < kPk; i++) pk[i] = 0;
-    if (!fa.ib_mask && !fa.nkill && !fa.bitmap_out) {  // count only: word order does not matter
+    // sharded path: this tile's super-block (slot), its parents and rank offset
+    const int64_t slot = fa.kill_tab || fa.rank_add_tab ? tile / fa.tiles_per_slot : 0;
+    const int64_t slot_blk0 = slot * fa.tiles_per_slot * nb;  // first block of the slot
+    const int64_t rank_add = fa.rank_add_tab ? fa.rank_add_tab[slot] - slot_blk0 * 243 : fa.rank_add;
+    const uint64_t *kills = fa.kill_tab ? fa.kill_tab + slot * kMaxKill : nullptr;
+    if (!fa.ib_mask && !kills && !fa.bitmap_out) {  // count only: word order does not matter
 #pragma unroll
         for (int j = 0; j < kMaxIter; j++) {
             const int b = b0 + 32 * j + lane;
@@ -96,13 +101,15 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                     x0 = make_uint4(v[0], v[1], v[2], v[3]);
                     x1 = make_uint4(v[4], v[5], v[6], v[7]);
                 }
-                if (fa.nkill) {
+                if (kills) {
                     // top-axis parents (sharded path): OR of up to kMaxKill
-                    // bitmaps read in place, local or peer memory over NVLink
+                    // super-blocks read in place, local or peer memory over NVLink
                     uint4 k0 = make_uint4(0, 0, 0, 0), k1 = k0;
 #pragma unroll 1
-                    for (int q = 0; q < fa.nkill; q++) {
-                        const uint4 *kq = reinterpret_cast<const uint4 *>(fa.kill[q] + (blk0 + b) * 8);
+                    for (int q = 0; q < kMaxKill && kills[q]; q++) {
+                        const uint4 *kq =
+                            reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(kills[q]) +
+                                                            (blk0 + b - slot_blk0) * 8);
                         const uint4 a0 = kq[0], a1 = kq[1];
                         k0 = make_uint4(k0.x | a0.x, k0.y | a0.y, k0.z | a0.z, k0.w | a0.w);
                         k1 = make_uint4(k1.x | a1.x, k1.y | a1.y, k1.z | a1.z, k1.w | a1.w);
@@ -110,7 +117,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
                     x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
                     x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
                 }
-                if (fa.ib_mask || fa.nkill) {
+                if (fa.ib_mask || kills) {
                     p[h] = h ? x1 : x0;
                     p[h ^ 1] = h ? x0 : x1;
                 }
@@ -215,7 +222,7 @@ __device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, co
         }
         int64_t pos = run + (incl - cnt);
         run += __shfl_sync(0xffffffffu, incl, 31);
-        const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+        const int64_t rbase = (blk0 + b) * 243 + rank_add;
         int64_t *o = fa.out + pos;
         if (pos + cnt <= fa.cap) {
             // walk only the nonzero words (most blocks hold one or two): their
@@ -288,6 +295,16 @@ __global__ void k_chunk_advance(const int32_t *__restrict__ cnt_last, const int6
 __global__ void k_scan_total(const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos, int64_t n,
                              int64_t *total) {
     if (threadIdx.x == 0 && blockIdx.x == 0) *total = n ? pos[n - 1] + cnt[n - 1] : 0;
+}
+
+// sharded path: the output range of each of nslots states (tps tiles each)
+__global__ void k_slot_spans(const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos, int64_t tps,
+                             int64_t nslots, int64_t *__restrict__ start, int64_t *__restrict__ count) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const int64_t a = pos[s * tps], e = (s + 1) * tps - 1;
+    start[s] = a;
+    count[s] = pos[e] + cnt[e] - a;
 }
 
 // Copy every tile's ranks from its scratch range to its rank-order position
@@ -422,7 +439,7 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     }
     __syncthreads();
     mbar_wait(&mbar, 0);
-    tile_reduce_c0_t<G, 0>(sm);
+    if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
     tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa);
 }
 
@@ -487,15 +504,16 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
               cudaStream_t s) {
     uint32_t *bitmap_out = o.bitmap_out;
     int64_t *count_dev = o.count_dev;
-    if (o.nkill < 0 || o.nkill > kMaxKill) return set_err(DQMC_ERR_INVALID, "too many kill bitmaps");
-    const uint64_t S = (uint64_t)p.nblocks * 32;
-    const int64_t ntiles = p.T == 0 ? 1 : pow3l(p.T);
+    const int64_t nbatch = std::max<int64_t>(1, o.nbatch);
+    const uint64_t S = (uint64_t)p.nblocks * 32 * nbatch;
+    const int64_t tps = p.T == 0 ? 1 : pow3l(p.T);  // tiles per state
+    const int64_t ntiles = tps * nbatch;
     const int tile_smem = (int)pow3l(p.g) * 32;
     int rc;
     if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
-    if ((o.nkill || bitmap_out) && p.T > 0 && p.pitch != pow3l(p.g))
+    if ((o.kill_tab || bitmap_out || nbatch > 1) && p.T > 0 && p.pitch != pow3l(p.g))
         return set_err(DQMC_ERR_INVALID, "internal: kill/bitmap outputs need the reference layout plan");
     const bool direct = ntiles == 1;  // one tile: its ranks are already in order
     if (!count_only && !direct) {
@@ -506,8 +524,10 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     fa.out = count_only ? nullptr : (direct ? ranks : g_eng.scratch);
     fa.cap = count_only ? 0 : (direct ? cap : (int64_t)g_eng.scratch_cap);
     fa.rank_add = rank_add;
-    fa.nkill = o.nkill;
-    for (int q = 0; q < o.nkill; q++) fa.kill[q] = o.kill[q];
+    fa.kill_tab = o.kill_tab;
+    fa.rank_add_tab = o.rank_add_tab;
+    fa.tiles_per_slot = tps;
+    fa.skip_c0 = o.skip_c0 ? 1 : 0;
     fa.ib_mask = ib_mask;
     fa.bitmap_out = bitmap_out;
     fa.alloc = g_eng.alloc;
@@ -525,7 +545,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
         CUtensorMap ma, mb;
         if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
         if ((rc = launch_c0_final(p.g, ntiles, state, fa, ma, mb, s))) return rc;
-        tm.mark("k_c0_final", S * (1 + o.nkill) + (bitmap_out ? S : 0));
+        tm.mark("k_c0_final", S + (bitmap_out ? S : 0));
     }
     if (ntiles <= 4096) {
         k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
@@ -542,6 +562,11 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
         CK(cudaGetLastError());
     }
     tm.mark("k_scan_tiles", (uint64_t)ntiles * 12);
+    if (o.slot_start && o.slot_count) {
+        k_slot_spans<<<(unsigned)((nbatch + 255) / 256), 256, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, tps, nbatch,
+                                                                       o.slot_start, o.slot_count);
+        CK(cudaGetLastError());
+    }
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
         k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos, ranks, cap,
@@ -580,7 +605,7 @@ int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, 
     int rc;
     if ((rc = run_final(p, tt32, state, ib_mask, rank_add, ranks, cap, count_only, o, count, tm, s))) return rc;
     if (o.count_dev) return DQMC_OK;  // async: the caller sees -(count + 1) and retries synchronously
-    const bool direct = (p.T == 0);
+    const bool direct = (p.T == 0) && o.nbatch <= 1;
     if (!count_only && !direct && (size_t)*count > g_eng.scratch_cap) {
         g_eng.scratch_want = (size_t)((double)*count * 1.05) + 1024;
         const bool on = tm.on;

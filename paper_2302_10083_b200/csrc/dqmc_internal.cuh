@@ -79,9 +79,14 @@ struct FinalArgs {
     int64_t *out;               // scratch (multi-tile) or final ranks (single tile); null = count only
     int64_t cap;                // capacity of out
     int64_t rank_add;           // added to every rank (dummy-variable padding < 0, top-block offset > 0)
-    const uint32_t *kill[kMaxKill] = {};  // optional: bitmaps whose OR is cleared after the low reduce
-                                          // (the top-axis parent blocks of the sharded path, local or peer)
-    int nkill = 0;
+    // sharded path: the state is nslots consecutive super-blocks (tiles_per_slot
+    // tiles each); per slot up to kMaxKill parent super-block addresses (null
+    // padded; local or peer memory) whose OR is cleared, and the rank added
+    // to the slot's cells (rank_add_tab; null: rank_add for every tile)
+    const uint64_t *kill_tab = nullptr;
+    const int64_t *rank_add_tab = nullptr;
+    int64_t tiles_per_slot = 1;
+    int skip_c0 = 0;            // the C0 axes are already reduced (sharded extract pass)
     uint32_t ib_mask;           // in-block axes reduced in this pass
     uint32_t *bitmap_out;       // write final bitmap here (null: do not)
     unsigned long long *alloc;  // running scratch allocation counter
@@ -492,15 +497,20 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
 
 // reduce passes C, D (dqmc_reduce.cu)
 int reduce_set_attrs();
-int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s);
+// nbatch: that many consecutive independent states of this plan (reduce-only)
+int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s, int64_t nbatch = 1);
 
 // final stage E (dqmc_final.cu)
 int final_set_attrs();
 struct FinalOpts {
-    const uint32_t *const *kill = nullptr;  // nkill parent bitmaps (reference layout), OR-ed and cleared
-    int nkill = 0;
     uint32_t *bitmap_out = nullptr;         // write the final bitmap (reference layout)
     int64_t *count_dev = nullptr;           // DQMC_FLAG_ASYNC: publish the count here, no host sync
+    int64_t nbatch = 1;                     // consecutive independent states (sharded super-blocks)
+    const uint64_t *kill_tab = nullptr;     // per state: kMaxKill parent addresses (FinalArgs.kill_tab)
+    const int64_t *rank_add_tab = nullptr;  // per state: rank of its first cell
+    bool skip_c0 = false;                   // the C0 axes are already reduced
+    int64_t *slot_start = nullptr;          // per state: offset / count of its ranks in the output
+    int64_t *slot_count = nullptr;
 };
 int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32_t ib_mask, int64_t rank_add,
               int64_t *ranks, int64_t cap, bool count_only, const FinalOpts &o, int64_t *count, Timer &tm,

@@ -399,8 +399,9 @@ int reduce_set_attrs() {
 // reduced in one pass (single-GPU plan); otherwise every group is reduce-only
 // (sharded path, M already complete). The in-block axes of pass C go with the
 // last group either way.
-int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s) {
-    const uint64_t S = (uint64_t)p.nblocks * 32;
+int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s, int64_t nbatch) {
+    const uint64_t S = (uint64_t)p.nblocks * 32 * nbatch;
+    if (nbatch > 1 && (fused || p.pm)) return set_err(DQMC_ERR_INVALID, "internal: batched reduce is reduce-only");
     int rc;
     {
         const int k = p.m - 1;
@@ -410,7 +411,7 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
             if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
             tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(S * std::pow(2.0 / 3.0, p.r[k]) + S));
         } else {
-            if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
+            if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, nbatch, p.ib_C, s))) return rc;
             tm.mark("k_strided<REDUCE>", 2 * S);
         }
     }
@@ -419,7 +420,8 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
-        if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above), p.ib_D[k], s, k == 0 && p.pm)))
+        if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above) * nbatch, p.ib_D[k], s,
+                                                k == 0 && p.pm)))
             return rc;
         tm.mark("k_strided<REDUCE>", 2 * S);
     }

@@ -25,15 +25,18 @@ The algorithm (composition verified on the reference):
      super-blocks are then, level by level (number of star GPU digits), the
      AND of their two children, one read in place from the peer over NVLink
      (block-level MERGE of dense.py:174-212, merge_triple dense.py:46-48).
-  2. REDUCE: super-block d's primes are REDUCE_low(M_d) AND NOT OR_i M_{d[i->*]}
-     over its fixed top digits i (oracle formula oracle.py:77-80; the parents
-     must be pre-REDUCE). The final pass reads the <= K parent super-blocks in
-     place (local or peer pointers) and applies the OR in registers: no kill
-     buffers, no staging copies. Levels run by the number of stars of d,
-     ascending, with a fence between levels: a super-block's readers (its
-     children) all belong to the level before its own, so it can be reduced
-     in place once that level is done.
-  3. Compaction per super-block, with its global rank offset.
+  2. REDUCE_low: every rank reduces the L low variables of all its
+     super-blocks in place, in one batched set of passes.
+  3. Primes of super-block d = R_low(M_d) AND NOT OR_i R_low(M_{d[i->*]}) over
+     its fixed top digits i (oracle formula oracle.py:77-80 with M_parent
+     replaced by R_low(M_parent): a parent cleared by one of its own low
+     parents means the cell's low parent along that axis is an implicant, so
+     the cell dies either way; the parents must NOT carry their own top
+     kills). One final pass over all of a rank's super-blocks reads the <= K
+     parents of each in place (local or peer pointers, a per-slot table) and
+     applies the OR in registers: no kill buffers, no staging copies, and one
+     fence between steps 2 and 3 instead of one per level.
+  4. Compaction with each super-block's global rank offset, slot by slot.
 NCCL has no bitwise-AND reduction (nccl.h ops: sum/prod/max/min/avg) and the
 exchange here is pure peer loads, so the only collectives are the level
 fences and the one-time exchange of arena IPC handles.
@@ -137,8 +140,10 @@ class ShardPlan:
                 self.slot[d] = nslots[g]
                 nslots[g] += 1
         self.nslots = nslots
+        self.slot_blocks = [[None] * nslots[g] for g in range(self.world)]  # rank -> super-block per slot
+        for d in self.blocks:
+            self.slot_blocks[self.owner[d]][self.slot[d]] = d
         self.merge_levels = self._merge_levels()
-        self.reduce_levels = self._reduce_levels()
 
     # -- layout
     def ref(self, d) -> Ref:
@@ -170,14 +175,9 @@ class ShardPlan:
             levels.append(jobs)
         return levels
 
-    def _reduce_levels(self):
-        """Level l (0..K): (d, parents) for every super-block with l stars; the
-        parents d[i->*] over its fixed digits are read pre-REDUCE (level l+1)."""
-        levels = [[] for _ in range(self.K + 1)]
-        for d in self.blocks:
-            parents = [d[:i] + (2,) + d[i + 1 :] for i in range(self.K) if d[i] != 2]
-            levels[sum(x == 2 for x in d)].append((d, parents))
-        return levels
+    def parents(self, d) -> list:
+        """The super-blocks d[i->*] over d's fixed digits (<= K <= MAX_KILL)."""
+        return [d[:i] + (2,) + d[i + 1 :] for i in range(self.K) if d[i] != 2]
 
     # -- budget
     def tile_bytes(self) -> int:
@@ -204,7 +204,7 @@ class ShardPlan:
             "arena_bytes": [self.arena_bytes(g) for g in range(self.world)],
             "peak_device_bytes": peaks, "max_peak_device_bytes": max(peaks),
             "balance": max(peaks) / (total / self.world),
-            "merge_levels": len(self.merge_levels), "reduce_levels": len(self.reduce_levels),
+            "merge_levels": len(self.merge_levels),
             "peer_read_bytes": recv,
         }
 
@@ -229,10 +229,9 @@ class ShardPlan:
             for d, c0, c1 in jobs:
                 g = self.owner[d]
                 out[g] += sum(self.sb_bytes for c in (c0, c1) if self.owner[c] != g)
-        for jobs in self.reduce_levels:
-            for d, parents in jobs:
-                g = self.owner[d]
-                out[g] += sum(self.sb_bytes for p in parents if self.owner[p] != g)
+        for d in self.blocks:
+            g = self.owner[d]
+            out[g] += sum(self.sb_bytes for p in self.parents(d) if self.owner[p] != g)
         return out
 
 
@@ -242,8 +241,8 @@ class ShardPlan:
 
 def run_schedule(plan: ShardPlan, inputs: dict, ops, comm, count_only: bool = False) -> dict:
     """Run the sharded call. ``inputs[g]`` is rank g's table slice for every
-    rank local to ``comm``. Returns {d: result of ops.reduce_extract} for the
-    super-blocks those ranks own."""
+    rank local to ``comm``. Returns {d: result} for the super-blocks those
+    ranks own: a (start, count) span of ops' rank output, or a count."""
     local = comm.local_ranks()
     for g in local:
         ops.ensure_arena(g, plan.arena_bytes(g))
@@ -252,18 +251,21 @@ def run_schedule(plan: ShardPlan, inputs: dict, ops, comm, count_only: bool = Fa
     for g in local:
         ops.merge(inputs[g], nl, Ref(g, 0))
     comm.fence(ops)
-    for jobs in plan.merge_levels:
-        for d, c0, c1 in jobs:
-            if plan.owner[d] in local:
-                ops.and_(plan.ref(d), plan.ref(c0), plan.ref(c1), plan.sb_bytes)
+    for jobs in plan.merge_levels:  # star super-blocks: one batched AND per level and rank
+        for g in local:
+            mine = [(plan.ref(d), plan.ref(c0), plan.ref(c1)) for d, c0, c1 in jobs if plan.owner[d] == g]
+            ops.and_batch(mine, plan.sb_bytes)
         comm.fence(ops)
+    for g in local:  # R_low of every super-block, in place
+        ops.reduce_low(g, plan.L, plan.nslots[g])
+    comm.fence(ops)  # parents are read only once every rank holds R_low
     out = {}
-    for jobs in plan.reduce_levels:
-        for d, parents in jobs:
-            if plan.owner[d] in local:
-                out[d] = ops.reduce_extract(plan.ref(d), plan.L, [plan.ref(p) for p in parents], plan.offset(d),
-                                            count_only)
-        comm.fence(ops)
+    for g in local:
+        slots = plan.slot_blocks[g]
+        kills = [[plan.ref(q) for q in plan.parents(d)] for d in slots]
+        res = ops.extract(g, plan.L, kills, [plan.offset(d) for d in slots], count_only)
+        out.update(zip(slots, res))
+    comm.fence(ops)  # nobody reads an arena once its owner may rewrite it (next call)
     return out
 
 
@@ -350,7 +352,7 @@ class ProcessComm:
 class GpuOps:
     """Super-block compute on the current CUDA device through the C ABI.
     Ranks of every super-block are written back to back into one device
-    buffer (``out``); reduce_extract returns the (start, count) span."""
+    buffer (``out``); extract returns their (start, count) spans."""
 
     def __init__(self, device=None):
         import torch
@@ -416,38 +418,56 @@ class GpuOps:
         kind = self._lib.IN_U8 if values.dtype == self.torch.uint8 else self._lib.IN_WORDS
         self._lib.check(self.L.dqmc_merge_device(values.data_ptr(), kind, nl, self.ptr(dst), self._stream()))
 
-    def and_(self, dst: Ref, a: Ref, b: Ref, nbytes: int):
-        self._lib.check(self.L.dqmc_bitop_device(self.ptr(dst), self.ptr(a), self.ptr(b), nbytes, 0, self._stream()))
+    def and_batch(self, triples, nbytes: int):
+        """dst = a & b for every (dst, a, b) of one merge level: one launch."""
+        if not triples:
+            return
+        t = self.torch
+        jobs = t.tensor([[self.ptr(d), self.ptr(a), self.ptr(b)] for d, a, b in triples], dtype=t.int64)
+        self._jobs = jobs.to(self.device, non_blocking=False)  # kept alive until the launch has read it
+        self._lib.check(self.L.dqmc_bitop_batch_device(self._jobs.data_ptr(), len(triples), nbytes, 0,
+                                                       self._stream()))
 
-    def reduce_extract(self, ref: Ref, L: int, kills: list, offset: int, count_only: bool):
+    def reduce_low(self, g: int, L: int, nslots: int):
+        self._lib.check(self.L.dqmc_reduce_low_device(self.bases[g], L, nslots, self._stream()))
+
+    def extract(self, g: int, L: int, kills: list, rank_adds: list, count_only: bool):
+        """Primes of rank g's nslots super-blocks: [(start, count)] spans of
+        ``out`` in slot order, or counts."""
         import ctypes
 
-        kp = (ctypes.c_void_p * max(1, len(kills)))(*[self.ptr(r) for r in kills])
-        cnt = ctypes.c_int64(0)
+        t = self.torch
+        nslots = len(kills)
+        key = (g, L, tuple(self.bases.items()))
+        if getattr(self, "_tab_key", None) != key:  # tables depend only on the plan and the arenas
+            tab = [[self.ptr(r) for r in ks] + [0] * (MAX_KILL - len(ks)) for ks in kills]
+            self._tab = t.tensor(tab, dtype=t.int64).to(self.device)
+            self._radd = t.tensor(rank_adds, dtype=t.int64).to(self.device)
+            self._spans = t.empty((2, nslots), dtype=t.int64, device=self.device)
+            self._tab_key = key
+        total = ctypes.c_int64(0)
         flags = self._lib.FLAG_COUNT_ONLY if count_only else 0
-        if count_only:
-            self._lib.check(self.L.dqmc_reduce_extract_device(self.ptr(ref), L, kp, len(kills), int(offset), None, 0,
-                                                              ctypes.byref(cnt), flags, self._stream()))
-            return int(cnt.value)
         if self.out is None:
-            self.out = self.torch.empty(1 << 22, dtype=self.torch.int64, device=self.device)
+            self.out = t.empty(1 << 22, dtype=t.int64, device=self.device)
         for _ in range(2):
-            free = self.out.numel() - self.cursor
-            dst = self.out.data_ptr() + 8 * self.cursor
-            self._lib.check(self.L.dqmc_reduce_extract_device(self.ptr(ref), L, kp, len(kills), int(offset), dst,
-                                                              free, ctypes.byref(cnt), flags, self._stream()))
-            c = int(cnt.value)
-            if c <= free:
+            free = 0 if count_only else self.out.numel() - self.cursor
+            dst = None if count_only else self.out.data_ptr() + 8 * self.cursor
+            self._lib.check(self.L.dqmc_extract_kills_device(
+                self.bases[g], L, nslots, self._tab.data_ptr(), self._radd.data_ptr(), dst, free,
+                self._spans[0].data_ptr(), self._spans[1].data_ptr(), ctypes.byref(total), flags, self._stream()))
+            if count_only or total.value <= free:
                 break
-            # grow the output and extract again: REDUCE is idempotent and the
-            # kills are read, never written, so the reduced block is reusable
-            bigger = self.torch.empty(max(2 * self.out.numel(), self.cursor + int(c * 1.25) + 1024),
-                                      dtype=self.torch.int64, device=self.device)
+            # grow the output and extract again (the arena is read, not written)
+            bigger = t.empty(max(2 * self.out.numel(), self.cursor + int(total.value * 1.25) + 1024),
+                             dtype=t.int64, device=self.device)
             bigger[: self.cursor].copy_(self.out[: self.cursor])
             self.out = bigger
-        span = (self.cursor, c)
-        self.cursor += c
-        return span
+        starts, counts = self._spans.cpu().tolist()
+        if count_only:
+            return counts
+        res = [(self.cursor + a, c) for a, c in zip(starts, counts)]
+        self.cursor += int(total.value)
+        return res
 
     def gather(self, parts: dict):
         """Device int64 ranks of the given super-blocks in global rank order."""

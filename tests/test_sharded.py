@@ -74,21 +74,28 @@ class CpuOps:
         st.run_pass(self.O.MERGE)
         self.words(dst, st.words.nbytes)[:] = st.words
 
-    def and_(self, dst, a, b, nbytes):
-        np.bitwise_and(self.words(a, nbytes), self.words(b, nbytes), out=self.words(dst, nbytes))
+    def and_batch(self, triples, nbytes):
+        for dst, a, b in triples:
+            np.bitwise_and(self.words(a, nbytes), self.words(b, nbytes), out=self.words(dst, nbytes))
 
-    def reduce_extract(self, ref, L, kills, offset, count_only):
+    def reduce_low(self, g, L, nslots):
         nb = self.O.state_bytes(L, 5)
-        w = self.words(ref, nb)
-        st = self.O.OracleState.from_words(w.copy(), L, 5)
-        st.run_pass(self.O.REDUCE)
-        w[:] = st.words  # reduced in place, as the GPU does
-        kill = np.zeros_like(st.words)
-        for p in kills:
-            kill |= self.words(p, nb)
-        st.words &= ~kill
-        r = st.extract_ranks() + offset
-        return len(r) if count_only else r
+        for s in range(nslots):
+            w = self.words(S.Ref(g, s * nb), nb)
+            st = self.O.OracleState.from_words(w.copy(), L, 5)
+            st.run_pass(self.O.REDUCE)
+            w[:] = st.words  # in place, as the GPU does
+
+    def extract(self, g, L, kills, rank_adds, count_only):
+        nb = self.O.state_bytes(L, 5)
+        res = []
+        for s, (ks, add) in enumerate(zip(kills, rank_adds)):
+            w = self.words(S.Ref(g, s * nb), nb).copy()
+            for q in ks:
+                w &= ~self.words(q, nb)
+            r = self.O.OracleState.from_words(w, L, 5).extract_ranks() + add
+            res.append(len(r) if count_only else r)
+        return res
 
 
 # ---------------------------------------------------------------------------
@@ -130,14 +137,14 @@ class TestPlan:
         assert done == set(p.blocks)
 
     @pytest.mark.parametrize("k", [1, 2, 3])
-    def test_reduce_parents_are_read_before_they_are_reduced(self, k):
+    def test_parents_exist_and_fit_the_kill_table(self, k):
         p = S.ShardPlan(16, k)
-        level = {d: lvl for lvl, jobs in enumerate(p.reduce_levels) for d, _ in jobs}
-        assert set(level) == set(p.blocks)
-        for lvl, jobs in enumerate(p.reduce_levels):
-            for d, parents in jobs:
-                assert len(parents) <= S.MAX_KILL
-                assert all(level[q] == lvl + 1 for q in parents)
+        for d in p.blocks:
+            ps = p.parents(d)
+            assert len(ps) == sum(x != 2 for x in d) <= S.MAX_KILL
+            assert all(q in p.owner for q in ps)
+        for g in range(p.world):  # slot lists cover each rank's arena exactly
+            assert [p.slot[d] for d in p.slot_blocks[g]] == list(range(p.nslots[g]))
 
     def test_super_blocks_tile_the_rank_space(self):
         p = S.ShardPlan(12, 2)
