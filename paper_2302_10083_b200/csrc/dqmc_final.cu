@@ -53,15 +53,15 @@ __device__ void tile_reduce_c0(uint32_t *sm, int g) {
 // one packed warp scan serves every group: the phases are short latency
 // chains, which is what bounds this pass (3 CTAs/SM, smem-limited).
 template <int NT>
-__device__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
+__device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
     constexpr int kMaxIter = ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;  // ceil(max warp range / 32)
     constexpr int kPk = (kMaxIter + 1) / 2;
     __shared__ int64_t s_warp_off[NT / 32];
     __shared__ int64_t s_tile_off;
     __shared__ uint16_t s_cnt[NT / 32][kMaxIter][32];  // slow-path block popcounts, then the emission list
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    const int b0 = (int)((int64_t)nb * warp / nwarps), b1 = (int)((int64_t)nb * (warp + 1) / nwarps);
+    constexpr int nwarps = NT / 32;  // compile-time: the range split needs no runtime division
+    const int b0 = nb * warp / nwarps, b1 = nb * (warp + 1) / nwarps;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
 
     // (1) lane = block: popcount (+ in-block axes, kills, bitmap on the slow path)
