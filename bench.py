@@ -24,6 +24,9 @@ inputs from the reference's frozen generator.
          it: the oracle port on 1 thread and on all threads, and the reference
          package itself (implicants.dense_prime_ranks, 1 thread) when it is
          installed in baseline/_ref.
+  next_rows  SURVEY.md §8(f) rows against the reference's own code: the GPU
+         sparse engine (f4) at low density, the device DenseState path (f2),
+         the on-device generator (f3).
   cpu_baseline  the oracle port (C restatement of the reference's dense
          engine, all host threads) on a bounded sample of the same workload,
          with the host CPU model and core count, the reference package's own
@@ -192,17 +195,32 @@ import json, sys, time
 import numpy as np
 sys.path.insert(0, sys.argv[1])
 sys.path.insert(1, sys.argv[2])
-from implicants import TruthTable, dense_prime_ranks
+from implicants import TruthTable, dense_prime_ranks, sparse_prime_ranks
+from implicants.dense import extract_ranks, load
 from oracle import gen as G
+
+
+def state_path(tt):  # load -> run_merge_reduce -> extract_ranks (dense.py:317-397)
+    st = load(tt)
+    st.run_merge_reduce()
+    return extract_ranks(st)
+
+
+ENG = {"dense": dense_prime_ranks, "sparse": sparse_prime_ranks, "state": state_path}
 out = {}
 for spec in json.loads(sys.argv[3]):
-    v = G.config_values(spec["cfg"], spec.get("n"))
-    n = len(v).bit_length() - 1
-    tt = TruthTable.from_bools(n, v != 0)
+    if "density" in spec:
+        n = spec["n"]
+        tt = TruthTable(n, G.random_words(n, spec["density"], spec["seed"]))
+    else:
+        v = G.config_values(spec["cfg"], spec.get("n"))
+        n = len(v).bit_length() - 1
+        tt = TruthTable.from_bools(n, v != 0)
+    f = ENG[spec.get("engine", "dense")]
     best, cnt = None, 0
     for _ in range(spec["reps"]):
         t0 = time.perf_counter()
-        r = dense_prime_ranks(tt)
+        r = f(tt)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
         cnt = len(r)
@@ -380,6 +398,72 @@ def bench_configs(args, pkg, device, _lib) -> dict:
     return out
 
 
+def bench_next_rows(args, pkg, device) -> dict:
+    """SURVEY.md §8(f) rows beside the reference's own implementation of each
+    (NumPy, 1 thread, baseline/_ref; min over reps, perf_counter around the
+    call only): f4 the sparse engine at low density, f2 the DenseState path
+    (load -> run_merge_reduce -> extract_ranks), f3 the input generator."""
+    import torch
+
+    from oracle import gen as G
+    from paper_2302_10083_b200 import state as ST
+
+    out = {}
+    cases = [("f4_sparse_n20_d0.1", 20, 0.1, 1), ("f4_sparse_n18_d0.3", 18, 0.3, 2)]
+    specs = []
+    for key, n, d, seed in cases:
+        tt = pkg.TruthTable(n, G.random_words(n, d, seed))
+        r = pkg.sparse_prime_ranks(tt)  # warm
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            r = pkg.sparse_prime_ranks(tt)
+            ts.append(time.perf_counter() - t0)
+        td = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            rd = pkg.dense_prime_ranks(tt)
+            td.append(time.perf_counter() - t0)
+        out[key] = {"n": n, "density": d, "primes": len(r), "gpu_sparse_ms": min(ts) * 1e3,
+                    "gpu_dense_ms": min(td) * 1e3, "sparse_equals_dense": bool(np.array_equal(r, rd))}
+        specs.append({"key": key, "n": n, "density": d, "seed": seed, "reps": 1, "engine": "sparse"})
+    # f2: the layer-by-layer DenseState on the device (mirror off), config 2
+    v = config_values_cpu(2)
+    tt2 = pkg.TruthTable.from_values(16, v)
+    ts = []
+    for _ in range(4):
+        t0 = time.perf_counter()
+        st = ST.load(tt2, mirror=False)
+        st.run_merge_reduce()
+        r = ST.extract_ranks(st)
+        ts.append(time.perf_counter() - t0)
+        del st
+    out["f2_state_config2"] = {"n": 16, "primes": len(r), "gpu_state_ms": min(ts[1:]) * 1e3}
+    specs.append({"key": "f2_state_config2", "cfg": 2, "reps": 2, "engine": "state"})
+    # f3: the frozen generator, config-4 size, on the device vs the NumPy restatement
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    vd = device.gen3_device(24, 0.75, 0.05, 3)
+    e0.record()
+    for _ in range(5):
+        vd = device.gen3_device(24, 0.75, 0.05, 3)
+    e1.record()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    G.gen3(24, 0.75, 0.05, 3)
+    tcpu = time.perf_counter() - t0
+    out["f3_generator_n24"] = {"values": 1 << 24, "gpu_ms": e0.elapsed_time(e1) / 5,
+                               "numpy_ms": tcpu * 1e3, "note": "oracle/gen.py restatement of ttio.py:331-378"}
+    ref = reference_numpy_times(specs) if not args.no_cpu else None
+    for sp in specs:
+        k = sp["key"]
+        if isinstance(ref, dict) and k in ref:
+            out[k]["reference_numpy_ms"] = ref[k]["seconds"] * 1e3
+            out[k]["reference_primes_match"] = ref[k]["primes"] == out[k]["primes"]
+        else:
+            out[k]["reference_numpy_ms"] = ref if isinstance(ref, dict) else None
+    return out
+
+
 def run_engine_bench(args):
     import torch
 
@@ -491,6 +575,7 @@ def run_engine_bench(args):
     # ---- BASELINE configs 1-3: wall time to all primes at n (the metric's
     #      second half), GPU beside the CPU
     configs = bench_configs(args, pkg, device, _lib)
+    next_rows = bench_next_rows(args, pkg, device)
 
     # ---- CPU baseline: oracle port on a bounded sample (rank 0, N=1)
     cpu = None
@@ -575,6 +660,7 @@ def run_engine_bench(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "configs": configs,
+        "next_rows": next_rows,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
