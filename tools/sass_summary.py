@@ -9,12 +9,14 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(REPO, "paper_2302_10083_b200", "libdqmc.so")
-HOT = ("k_strided_pipe<3, 3, 2>", "k_merge_reduce_pipe<3, 3>", "k_c0_final<7>")
+HOT = ("k_strided_pipe<3, 3>", "k_merge_reduce_pipe<3, 3>", "k_c0_final<7>", "k_sp_generate")
 KEYS = ["LOP3", "SHF", "LDS", "STS", "LDG", "STG", "UTMALDG", "UTMASTG", "UBLKCP", "LDGSTS", "SYNCS", "POPC",
         "SHFL", "BAR", "IMAD", "IADD3", "ATOMG", "REDG"]
 
 
 def main():
+    if len(sys.argv) != 3 or not all(a.endswith((".md", ".txt")) for a in sys.argv[1:]):
+        sys.exit("usage: sass_summary.py <out>.md <out>.txt (outputs only; reads libdqmc.so)")
     txt = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", txt)
     out = ["# SASS evidence (cuobjdump -sass paper_2302_10083_b200/libdqmc.so, sm_100a)", "",
