@@ -622,11 +622,13 @@ void dqmc_release(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_eng.device < 0) return;
     cudaDeviceSynchronize();  // nothing in flight may still use the workspace
+    sparse_release();
     cudaFree(g_eng.state);
     cudaFree(g_eng.tile_base);
     cudaFree(g_eng.tile_pos);
     cudaFree(g_eng.tile_cnt);
     cudaFree(g_eng.scratch);
+    cudaFree(g_eng.tile_rank0);
     cudaFree(g_eng.alloc);
     cudaFree(g_eng.cub_tmp);
     cudaFree(g_eng.total);

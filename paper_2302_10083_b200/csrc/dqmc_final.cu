@@ -176,10 +176,11 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
         const int64_t base = acc ? (int64_t)atomicAdd(fa.alloc, (unsigned long long)acc) : 0;
         fa.tile_base[tile] = base;
         fa.tile_cnt[tile] = (int32_t)acc;
+        if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + rank_add;
         s_tile_off = base;
     }
     __syncthreads();
-    if (fa.out == nullptr) return;
+    if (fa.out == nullptr && fa.out32 == nullptr) return;
 
     // (4) ordered emission. Primes are sparse (~0.2 per block at n = 24, ~5
     //     nonzero blocks per 32-block group), so the nonzero blocks of the
@@ -222,8 +223,10 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
         }
         int64_t pos = run + (incl - cnt);
         run += __shfl_sync(0xffffffffu, incl, 31);
+        // scratch mode: 4-byte tile-relative offsets (k_reorder adds the tile's
+        // first rank), half the bytes of int64 ranks; single tile: final ranks
+        const uint32_t lbase = (uint32_t)b * 243u;
         const int64_t rbase = (blk0 + b) * 243 + rank_add;
-        int64_t *o = fa.out + pos;
         if (pos + cnt <= fa.cap) {
             // walk only the nonzero words (most blocks hold one or two): their
             // mask from the registers, the words themselves re-read from smem
@@ -231,21 +234,40 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
 #pragma unroll
             for (int k = 0; k < 8; k++) nz |= (wv[k] != 0u ? 1u : 0u) << k;
             const uint32_t *bw = sm + b * 8;
-            while (nz) {
-                const int k = __ffs(nz) - 1;
-                nz &= nz - 1;
-                uint32_t w = bw[k];
-                do {
-                    *o++ = rbase + k * 32 + (__ffs(w) - 1);
-                    w &= w - 1;
-                } while (w);
+            if (fa.out32) {
+                uint32_t *o = fa.out32 + pos;
+                while (nz) {
+                    const int k = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    uint32_t w = bw[k];
+                    do {
+                        *o++ = lbase + k * 32 + (__ffs(w) - 1);
+                        w &= w - 1;
+                    } while (w);
+                }
+            } else {
+                int64_t *o = fa.out + pos;
+                while (nz) {
+                    const int k = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    uint32_t w = bw[k];
+                    do {
+                        *o++ = rbase + k * 32 + (__ffs(w) - 1);
+                        w &= w - 1;
+                    } while (w);
+                }
             }
-        } else {  // the scratch is too small: write what fits (the host grows it and reruns)
+        } else {  // the output is too small: write what fits (the host grows it and reruns)
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 uint32_t w = wv[k];
                 while (w) {
-                    if (pos < fa.cap) fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                    if (pos < fa.cap) {
+                        if (fa.out32)
+                            fa.out32[pos] = lbase + k * 32 + (__ffs(w) - 1);
+                        else
+                            fa.out[pos] = rbase + k * 32 + (__ffs(w) - 1);
+                    }
                     pos++;
                     w &= w - 1;
                 }
@@ -316,17 +338,18 @@ __global__ void k_publish_count(const int64_t *__restrict__ total, int64_t limit
     *dst = t <= limit ? t : -(t + 1);
 }
 
-__global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scratch, const int64_t *__restrict__ base,
+__global__ void __launch_bounds__(256) k_reorder(const uint32_t *__restrict__ scratch, const int64_t *__restrict__ base,
                                                  const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
-                                                 int64_t *__restrict__ out, int64_t cap, int64_t ntiles,
-                                                 int64_t scap, const int64_t *__restrict__ dbase = nullptr) {
+                                                 const int64_t *__restrict__ rank0, int64_t *__restrict__ out,
+                                                 int64_t cap, int64_t ntiles, int64_t scap,
+                                                 const int64_t *__restrict__ dbase = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t add = dbase ? *dbase : 0;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
     for (int64_t t = w; t < ntiles; t += nw) {
         const int c = cnt[t];
-        const int64_t src = base[t], dst = pos[t] + add;
+        const int64_t src = base[t], dst = pos[t] + add, r0 = rank0[t];
         // a tile whose range overflowed the scratch is skipped: the host sees
         // total > scratch capacity, grows the scratch and reruns the final stage
         if (c < 0 || src < 0 || src + c > scap) continue;
@@ -334,16 +357,16 @@ __global__ void __launch_bounds__(256) k_reorder(const int64_t *__restrict__ scr
         if (dst + c <= cap) {
             // four independent loads in flight per lane (the copy is latency-bound)
             for (; i + 96 < c; i += 128) {
-                const int64_t a0 = __ldcs(scratch + src + i), a1 = __ldcs(scratch + src + i + 32);
-                const int64_t a2 = __ldcs(scratch + src + i + 64), a3 = __ldcs(scratch + src + i + 96);
-                out[dst + i] = a0;
-                out[dst + i + 32] = a1;
-                out[dst + i + 64] = a2;
-                out[dst + i + 96] = a3;
+                const uint32_t a0 = __ldcs(scratch + src + i), a1 = __ldcs(scratch + src + i + 32);
+                const uint32_t a2 = __ldcs(scratch + src + i + 64), a3 = __ldcs(scratch + src + i + 96);
+                out[dst + i] = r0 + a0;
+                out[dst + i + 32] = r0 + a1;
+                out[dst + i + 64] = r0 + a2;
+                out[dst + i + 96] = r0 + a3;
             }
         }
         for (; i < c; i += 32)
-            if (dst + i < cap) out[dst + i] = __ldcs(scratch + src + i);
+            if (dst + i < cap) out[dst + i] = r0 + __ldcs(scratch + src + i);
     }
 }
 
@@ -518,10 +541,13 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     const bool direct = ntiles == 1;  // one tile: its ranks are already in order
     if (!count_only && !direct) {
         const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
-        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 4))) return rc;
+        if ((rc = grow(g_eng.tile_rank0, g_eng.tile_rank0_cap, (size_t)ntiles, 8))) return rc;
     }
     FinalArgs fa;
-    fa.out = count_only ? nullptr : (direct ? ranks : g_eng.scratch);
+    fa.out = count_only || !direct ? nullptr : ranks;
+    fa.out32 = count_only || direct ? nullptr : g_eng.scratch;
+    fa.tile_rank0 = fa.out32 ? g_eng.tile_rank0 : nullptr;
     fa.cap = count_only ? 0 : (direct ? cap : (int64_t)g_eng.scratch_cap);
     fa.rank_add = rank_add;
     fa.kill_tab = o.kill_tab;
@@ -569,8 +595,8 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     }
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
-        k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos, ranks, cap,
-                                       ntiles, (int64_t)g_eng.scratch_cap);
+        k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos,
+                                       g_eng.tile_rank0, ranks, cap, ntiles, (int64_t)g_eng.scratch_cap);
         CK(cudaGetLastError());
         tm.mark("k_reorder", (uint64_t)ntiles * 16);
     }
@@ -591,8 +617,11 @@ namespace {
 void add_rank_bytes(Timer &tm, int64_t written) {
     if (tm.bytes.empty()) return;
     for (size_t i = 0; i < tm.names.size(); i++) {
-        if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += (uint64_t)written * 8;
-        if (tm.names[i] == "k_reorder") tm.bytes[i] += (uint64_t)written * 16;
+        // E writes 4-B tile-relative offsets when k_reorder follows (multi-tile),
+        // final 8-B ranks otherwise; k_reorder reads 4 B and writes 8 B per rank
+        const bool multi = std::find(tm.names.begin(), tm.names.end(), "k_reorder") != tm.names.end();
+        if (tm.names[i] == "k_c0_final" || tm.names[i] == "k_small") tm.bytes[i] += (uint64_t)written * (multi ? 4 : 8);
+        if (tm.names[i] == "k_reorder") tm.bytes[i] += (uint64_t)written * 12;
     }
 }
 }  // namespace
@@ -638,9 +667,12 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
     int64_t *hbase = g_eng.hbase;  // mapped pinned mirror of the chunk bases
     for (int attempt = 0; attempt < 2; attempt++) {
         const size_t want = std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
-        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 8))) return rc;
+        if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 4))) return rc;
+        if ((rc = grow(g_eng.tile_rank0, g_eng.tile_rank0_cap, (size_t)ntiles, 8))) return rc;
         FinalArgs fa;
-        fa.out = g_eng.scratch;
+        fa.out = nullptr;
+        fa.out32 = g_eng.scratch;
+        fa.tile_rank0 = g_eng.tile_rank0;
         fa.cap = (int64_t)g_eng.scratch_cap;
         fa.rank_add = -p.rank_sub;
         fa.ib_mask = p.ib_E;
@@ -669,7 +701,7 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
             CK(cudaGetLastError());
             const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 8);
             k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
-                                           g_eng.tile_pos + t0, g_eng.ranks, host_cap, t1 - t0,
+                                           g_eng.tile_pos + t0, g_eng.tile_rank0 + t0, g_eng.ranks, host_cap, t1 - t0,
                                            (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
             CK(cudaGetLastError());
             CK(cudaEventRecord(g_eng.chunk_ev[c], s));

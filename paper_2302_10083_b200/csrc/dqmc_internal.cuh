@@ -76,7 +76,10 @@ __device__ __forceinline__ int64_t bin_to_tern_rt(uint64_t b) {
 }
 
 struct FinalArgs {
-    int64_t *out;               // scratch (multi-tile) or final ranks (single tile); null = count only
+    int64_t *out;               // final ranks (single tile); null = scratch output or count only
+    uint32_t *out32 = nullptr;  // multi-tile: tile-relative cell offsets (< 3^12) into the scratch;
+                                // k_reorder adds the tile's first rank (tile_rank0) on the way out
+    int64_t *tile_rank0 = nullptr;
     int64_t cap;                // capacity of out
     int64_t rank_add;           // added to every rank (dummy-variable padding < 0, top-block offset > 0)
     // sharded path: the state is nslots consecutive super-blocks (tiles_per_slot
@@ -358,8 +361,10 @@ struct Engine {
     int64_t *tile_base = nullptr, *tile_pos = nullptr;
     int32_t *tile_cnt = nullptr;
     size_t tile_cap = 0, tile_pos_cap = 0, tile_cnt_cap = 0;  // entries
-    int64_t *scratch = nullptr;
+    uint32_t *scratch = nullptr;               // tile-relative offsets of the final stage
     size_t scratch_cap = 0, scratch_want = 0;  // entries
+    int64_t *tile_rank0 = nullptr;             // per tile: rank of its first cell
+    size_t tile_rank0_cap = 0;                 // entries
     unsigned long long *alloc = nullptr;
     int64_t *total = nullptr;
     void *cub_tmp = nullptr;
@@ -487,6 +492,9 @@ int validate(int n, int h);
 // engine_done(s) after the last enqueue that touches it
 int engine_begin(cudaStream_t s);
 int engine_done(cudaStream_t s);
+
+int alloc_pinned(size_t entries, PinnedBuf &out);  // pinned host pool (dqmc_free_result returns to it)
+void sparse_release();                              // the sparse engine's buffers (dqmc_sparse.cu)
 
 // input (dqmc_input.cu)
 int input_words(const void *in, int kind, int n, const uint32_t **tt32, cudaStream_t s);

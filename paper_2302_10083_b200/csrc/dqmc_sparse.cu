@@ -171,7 +171,15 @@ int64_t table_size(int64_t entries) {
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;  // bytes
-    ~DevBuf() { cudaFree(p); }
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
     int ensure(size_t bytes) {
         if (bytes <= cap && p) return DQMC_OK;
         cudaFree(p);
@@ -186,6 +194,11 @@ struct DevBuf {
         return DQMC_OK;
     }
 };
+
+struct SparseWork {
+    DevBuf tt, ctr, tabA, tabB, cand, ranks, sorted, tmp;
+};
+SparseWork g_sp;
 
 int refuse_table(int64_t size, uint64_t cap) {
     char buf[256];
@@ -212,7 +225,10 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
         mem_cap = (uint64_t)((double)fr * 0.75);
     }
     const int64_t nwords = std::max<int64_t>(1, (1ll << n) / 64);
-    DevBuf tt, ctr, tabA, tabB, cand, ranks;
+    // grow-only buffers kept across calls (released by dqmc_release): no
+    // cudaMalloc/cudaFree (device-wide syncs) on the steady-state path
+    DevBuf &tt = g_sp.tt, &ctr = g_sp.ctr, &tabA = g_sp.tabA, &tabB = g_sp.tabB, &cand = g_sp.cand,
+           &ranks = g_sp.ranks;
     if ((rc = tt.ensure((size_t)nwords * 8)) || (rc = ctr.ensure(64))) return rc;
     unsigned long long *cnt = (unsigned long long *)ctr.p;
     CK(cudaMemcpyAsync(tt.p, tt_host, (size_t)nwords * 8, cudaMemcpyHostToDevice, s));
@@ -288,7 +304,7 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
     out->ranks = nullptr;
     out->_owner = nullptr;
     if (total == 0) return DQMC_OK;
-    DevBuf sorted, tmp;
+    DevBuf &sorted = g_sp.sorted, &tmp = g_sp.tmp;
     size_t tmpb = 0;
     if ((rc = sorted.ensure((size_t)total * 8))) return rc;
     int bits = 1;
@@ -296,19 +312,22 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
     CK(cub::DeviceRadixSort::SortKeys(nullptr, tmpb, (const int64_t *)ranks.p, (int64_t *)sorted.p, total, 0, bits, s));
     if ((rc = tmp.ensure(tmpb))) return rc;
     CK(cub::DeviceRadixSort::SortKeys(tmp.p, tmpb, (const int64_t *)ranks.p, (int64_t *)sorted.p, total, 0, bits, s));
-    int64_t *host = nullptr;
-    CK(cudaHostAlloc((void **)&host, (size_t)total * 8, cudaHostAllocDefault));
-    CK(cudaMemcpyAsync(host, sorted.p, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
+    PinnedBuf pb;  // from the engine's pinned pool (dqmc_free_result returns it)
+    if ((rc = alloc_pinned((size_t)total, pb))) return rc;
+    CK(cudaMemcpyAsync(pb.ptr, sorted.p, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    PinnedBuf *pb = new PinnedBuf();
-    pb->ptr = host;
-    pb->cap = (size_t)total;
-    out->ranks = host;
-    out->_owner = pb;
+    out->ranks = pb.ptr;
+    out->_owner = new PinnedBuf(pb);
     return DQMC_OK;
 }
 
 }  // namespace
+
+void sparse_release() {
+    for (DevBuf *b : {&g_sp.tt, &g_sp.ctr, &g_sp.tabA, &g_sp.tabB, &g_sp.cand, &g_sp.ranks, &g_sp.sorted, &g_sp.tmp})
+        b->release();
+}
+
 }  // namespace dqmc
 
 using namespace dqmc;
