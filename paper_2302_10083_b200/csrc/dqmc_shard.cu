@@ -110,13 +110,13 @@ int dqmc_merge_device(const void *input_dev, int in_kind, int n, uint32_t *state
     return engine_done(s);
 }
 
-// REDUCE of the n low dimensions of nslots consecutive super-blocks, in place
-// (passes C/D as reduce-only over all slots, then pass E writing its reduced
-// tile back; no compaction, no host synchronisation). Afterwards every slot
-// holds R_low(M): that is what the extract pass reads as a parent (a cell's
-// kill by a low-reduced parent equals its kill by the parent's M, because a
-// parent cleared by one of its low parents implies the cell's own low parent
-// is an implicant — DESIGN.md §6).
+// REDUCE of the strided groups (and their in-block axes) of nslots
+// consecutive super-blocks, in place: passes C/D as reduce-only, batched over
+// the slots. The C0 and remaining in-block axes are reduced inside the
+// extract pass, on the tile in shared memory. A parent read as a kill source
+// may be reduced along any subset of its low axes: a parent cell cleared by
+// one of its own low parents implies the cell's own low parent along that
+// axis is an implicant, so the cell dies anyway.
 int dqmc_reduce_low_device(uint32_t *arena, int n, int64_t nslots, void *stream) {
     int rc;
     if ((rc = validate(n, 0))) return rc;
@@ -127,23 +127,20 @@ int dqmc_reduce_low_device(uint32_t *arena, int n, int64_t nslots, void *stream)
     if ((rc = ensure_attrs())) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     const Plan p = make_plan(n, false);     // caller-owned states in the reference layout
+    if (p.T == 0) return DQMC_OK;           // one tile per state: the extract pass does everything
     Timer tm{false, s};
     if ((rc = engine_begin(s))) return rc;
-    if (p.T > 0 && (rc = run_reduce(p, arena, false, tm, s, nslots))) return rc;
-    FinalOpts fo;
-    fo.bitmap_out = arena;
-    fo.nbatch = nslots;
-    fo.count_dev = g_eng.total + 20;  // count unused: keep the stream free of host syncs
-    int64_t unused = 0;
-    if ((rc = run_final(p, nullptr, arena, p.ib_E, 0, nullptr, 0, true, fo, &unused, tm, s))) return rc;
+    if ((rc = run_reduce(p, arena, false, tm, s, nslots))) return rc;
     return engine_done(s);
 }
 
-// Primes of nslots low-reduced super-blocks (dqmc_reduce_low_device): every
-// tile clears the OR of its slot's parent super-blocks (kill_tab: nslots x 8
-// device addresses, null padded; local or IPC peer memory) and emits its
-// ranks (+ rank_add[slot]). Ranks go out in slot order; slot_start/slot_count
-// (device, nslots each) give each slot's range; *total_out the sum (host).
+// Primes of nslots super-blocks after dqmc_reduce_low_device: every tile
+// finishes its low REDUCE in shared memory (the C0 axes and the remaining
+// in-block axes), clears the OR of its slot's parent super-blocks (kill_tab:
+// nslots x 8 device addresses, null padded; local or IPC peer memory) and
+// emits its ranks (+ rank_add[slot]). Ranks go out in slot order;
+// slot_start/slot_count (device, nslots each) give each slot's range;
+// *total_out the sum (host).
 int dqmc_extract_kills_device(const uint32_t *arena, int n, int64_t nslots, const uint64_t *kill_tab,
                               const int64_t *rank_add, int64_t *ranks_dev, int64_t ranks_cap, int64_t *slot_start,
                               int64_t *slot_count, int64_t *total_out, uint32_t flags, void *stream) {
@@ -165,10 +162,9 @@ int dqmc_extract_kills_device(const uint32_t *arena, int n, int64_t nslots, cons
     fo.nbatch = nslots;
     fo.kill_tab = kill_tab;
     fo.rank_add_tab = rank_add;
-    fo.skip_c0 = true;
     fo.slot_start = slot_start;
     fo.slot_count = slot_count;
-    if ((rc = run_final_retry(p, nullptr, arena, 0, 0, ranks_dev, ranks_cap, count_only, fo, total_out, tm, s)))
+    if ((rc = run_final_retry(p, nullptr, arena, p.ib_E, 0, ranks_dev, ranks_cap, count_only, fo, total_out, tm, s)))
         return rc;
     if ((rc = engine_done(s))) return rc;
     tm.finish();

@@ -25,17 +25,21 @@ The algorithm (composition verified on the reference):
      super-blocks are then, level by level (number of star GPU digits), the
      AND of their two children, one read in place from the peer over NVLink
      (block-level MERGE of dense.py:174-212, merge_triple dense.py:46-48).
-  2. REDUCE_low: every rank reduces the L low variables of all its
-     super-blocks in place, in one batched set of passes.
-  3. Primes of super-block d = R_low(M_d) AND NOT OR_i R_low(M_{d[i->*]}) over
-     its fixed top digits i (oracle formula oracle.py:77-80 with M_parent
-     replaced by R_low(M_parent): a parent cleared by one of its own low
-     parents means the cell's low parent along that axis is an implicant, so
-     the cell dies either way; the parents must NOT carry their own top
-     kills). One final pass over all of a rank's super-blocks reads the <= K
-     parents of each in place (local or peer pointers, a per-slot table) and
-     applies the OR in registers: no kill buffers, no staging copies, and one
-     fence between steps 2 and 3 instead of one per level.
+  2. REDUCE of the strided low groups: every rank reduces them for all its
+     super-blocks in place, in one batched set of passes — its own cube over
+     all n-k variables (its local-digit parents are inside it, and no other
+     super-block reads it as a parent), the star super-blocks over L.
+  3. Primes of super-block d = R_low(M_d) AND NOT OR_i R_A(M_{d[i->*]}) over
+     its fixed top digits i (own-cube super-blocks: only the GPU digits), where
+     R_A is the partial low REDUCE of step 2
+     (oracle formula oracle.py:77-80 with M_parent replaced by any partial
+     low REDUCE of it: a parent cleared by one of its own low parents means
+     the cell's low parent along that axis is an implicant, so the cell dies
+     either way; the parents must NOT carry their own top kills). One final
+     pass over all of a rank's super-blocks finishes each tile's low REDUCE
+     in shared memory, reads the <= K parents in place (local or peer
+     pointers, a per-slot table) and applies their OR in registers: no kill
+     buffers, no staging copies, and one fence between steps 2 and 3.
   4. Compaction with each super-block's global rank offset, slot by slot.
 NCCL has no bitwise-AND reduction (nccl.h ops: sum/prod/max/min/avg) and the
 exchange here is pure peer loads, so the only collectives are the level
@@ -179,6 +183,27 @@ class ShardPlan:
         """The super-blocks d[i->*] over d's fixed digits (<= K <= MAX_KILL)."""
         return [d[:i] + (2,) + d[i + 1 :] for i in range(self.K) if d[i] != 2]
 
+    def is_own(self, d) -> bool:
+        """d lies in its owner's own cube (binary GPU digits)."""
+        return 2 not in d[self.m :]
+
+    @property
+    def own_full(self) -> bool:
+        """The own cube's strided low groups cover every variable above the
+        super-blocks' 3^7-block C0 tile (L >= 12: both plans share that tile),
+        so reduce_low can reduce the own cube over all its n-k variables."""
+        return self.L >= 12 and self.m > 0
+
+    def kill_parents(self, d) -> list:
+        """The parents the extract pass reads for d. With own_full, a rank's
+        own cube is reduced over all its n-k variables in place (its
+        local-digit parents are inside it, and no other super-block reads it
+        as a parent), so its super-blocks only need their GPU-digit parents;
+        star super-blocks need every fixed digit's parent."""
+        if self.own_full and self.is_own(d):
+            return [d[:i] + (2,) + d[i + 1 :] for i in range(self.m, self.K) if d[i] != 2]
+        return self.parents(d)
+
     # -- budget
     def tile_bytes(self) -> int:
         """Engine tile arrays of one super-block's final pass (20 B per C0 tile)."""
@@ -231,7 +256,7 @@ class ShardPlan:
                 out[g] += sum(self.sb_bytes for c in (c0, c1) if self.owner[c] != g)
         for d in self.blocks:
             g = self.owner[d]
-            out[g] += sum(self.sb_bytes for p in self.parents(d) if self.owner[p] != g)
+            out[g] += sum(self.sb_bytes for p in self.kill_parents(d) if self.owner[p] != g)
         return out
 
 
@@ -256,13 +281,17 @@ def run_schedule(plan: ShardPlan, inputs: dict, ops, comm, count_only: bool = Fa
             mine = [(plan.ref(d), plan.ref(c0), plan.ref(c1)) for d, c0, c1 in jobs if plan.owner[d] == g]
             ops.and_batch(mine, plan.sb_bytes)
         comm.fence(ops)
-    for g in local:  # R_low of every super-block, in place
-        ops.reduce_low(g, plan.L, plan.nslots[g])
-    comm.fence(ops)  # parents are read only once every rank holds R_low
+    own = 3**plan.m if plan.own_full else 0
+    for g in local:  # strided low groups, in place: the own cube over all its n-k variables, the rest over L
+        if own:
+            ops.reduce_low(g, nl, 1, 0)
+        if plan.nslots[g] > own:
+            ops.reduce_low(g, plan.L, plan.nslots[g] - own, own * plan.sb_bytes)
+    comm.fence(ops)  # parents are read only once every rank has reduced them
     out = {}
     for g in local:
         slots = plan.slot_blocks[g]
-        kills = [[plan.ref(q) for q in plan.parents(d)] for d in slots]
+        kills = [[plan.ref(q) for q in plan.kill_parents(d)] for d in slots]
         res = ops.extract(g, plan.L, kills, [plan.offset(d) for d in slots], count_only)
         out.update(zip(slots, res))
     comm.fence(ops)  # nobody reads an arena once its owner may rewrite it (next call)
@@ -428,8 +457,8 @@ class GpuOps:
         self._lib.check(self.L.dqmc_bitop_batch_device(self._jobs.data_ptr(), len(triples), nbytes, 0,
                                                        self._stream()))
 
-    def reduce_low(self, g: int, L: int, nslots: int):
-        self._lib.check(self.L.dqmc_reduce_low_device(self.bases[g], L, nslots, self._stream()))
+    def reduce_low(self, g: int, n: int, nstates: int, off: int):
+        self._lib.check(self.L.dqmc_reduce_low_device(self.bases[g] + off, n, nstates, self._stream()))
 
     def extract(self, g: int, L: int, kills: list, rank_adds: list, count_only: bool):
         """Primes of rank g's nslots super-blocks: [(start, count)] spans of

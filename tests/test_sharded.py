@@ -78,20 +78,33 @@ class CpuOps:
         for dst, a, b in triples:
             np.bitwise_and(self.words(a, nbytes), self.words(b, nbytes), out=self.words(dst, nbytes))
 
-    def reduce_low(self, g, L, nslots):
-        nb = self.O.state_bytes(L, 5)
-        for s in range(nslots):
-            w = self.words(S.Ref(g, s * nb), nb)
-            st = self.O.OracleState.from_words(w.copy(), L, 5)
-            st.run_pass(self.O.REDUCE)
+    @staticmethod
+    def _split(L):
+        """As the GPU: reduce_low covers the strided groups (block digits above
+        the 3^min(L-5, 7)-block C0 tile), extract the C0 and in-block dims."""
+        c0 = 5 + min(L - 5, 7)
+        return list(range(c0 + 1, L + 1)), list(range(1, c0 + 1))
+
+    def reduce_low(self, g, n, nstates, off):
+        nb = self.O.state_bytes(n, 5)
+        groups, _ = self._split(n)
+        if not groups:
+            return
+        for s in range(nstates):
+            w = self.words(S.Ref(g, off + s * nb), nb)
+            st = self.O.OracleState.from_words(w.copy(), n, 5)
+            st.run_pass(self.O.REDUCE, dims=groups)
             w[:] = st.words  # in place, as the GPU does
 
     def extract(self, g, L, kills, rank_adds, count_only):
         nb = self.O.state_bytes(L, 5)
+        _, rest = self._split(L)
         res = []
         for s, (ks, add) in enumerate(zip(kills, rank_adds)):
-            w = self.words(S.Ref(g, s * nb), nb).copy()
-            for q in ks:
+            st = self.O.OracleState.from_words(self.words(S.Ref(g, s * nb), nb).copy(), L, 5)
+            st.run_pass(self.O.REDUCE, dims=rest)  # finish the low REDUCE (not written back)
+            w = st.words
+            for q in ks:  # parents as they are: only partially low-reduced
                 w &= ~self.words(q, nb)
             r = self.O.OracleState.from_words(w, L, 5).extract_ranks() + add
             res.append(len(r) if count_only else r)
@@ -136,15 +149,26 @@ class TestPlan:
             done |= {d for d, _, _ in jobs}
         assert done == set(p.blocks)
 
-    @pytest.mark.parametrize("k", [1, 2, 3])
-    def test_parents_exist_and_fit_the_kill_table(self, k):
-        p = S.ShardPlan(16, k)
+    @pytest.mark.parametrize("n,k", [(16, 1), (16, 2), (16, 3), (22, 2), (24, 3)])
+    def test_parents_exist_and_fit_the_kill_table(self, n, k):
+        p = S.ShardPlan(n, k)
+        read = set()
         for d in p.blocks:
             ps = p.parents(d)
             assert len(ps) == sum(x != 2 for x in d) <= S.MAX_KILL
             assert all(q in p.owner for q in ps)
+            kp = p.kill_parents(d)
+            assert set(kp) <= set(ps) and (kp == ps or (p.own_full and p.is_own(d)))
+            read |= set(kp)
+        # with own_full the own cubes are reduced over all their variables in place: nobody may read them
+        if p.own_full:
+            assert not any(p.is_own(q) for q in read)
         for g in range(p.world):  # slot lists cover each rank's arena exactly
             assert [p.slot[d] for d in p.slot_blocks[g]] == list(range(p.nslots[g]))
+
+    def test_own_cube_full_reduce_only_with_a_shared_c0_tile(self):
+        assert S.ShardPlan(27, 3).own_full and S.ShardPlan(24, 3).own_full
+        assert not S.ShardPlan(16, 2).own_full  # L = 10: the own cube's C0 tile differs
 
     def test_super_blocks_tile_the_rank_space(self):
         p = S.ShardPlan(12, 2)
@@ -197,7 +221,8 @@ class TestPlan:
 # the schedule on CPU
 
 
-@pytest.mark.parametrize("n,k,m", [(8, 1, None), (9, 2, None), (10, 3, None), (11, 2, 2), (12, 3, 3), (11, 1, 0)])
+@pytest.mark.parametrize("n,k,m", [(8, 1, None), (9, 2, None), (10, 3, None), (11, 2, 2), (12, 3, 3), (11, 1, 0),
+                                   (15, 1, 1), (16, 2, 1), (14, 1, 1)])
 def test_emulated_cpu_matches_single_engine(n, k, m, oracle_mod, gen_mod):
     v = gen_mod.gen3(n, 0.7, 0.1, n)
     plan = S.ShardPlan(n, k, m)
@@ -372,3 +397,24 @@ def test_bench_torchrun_two_ranks_gloo(tmp_path, pkg):
     want = len(pkg.prime_ranks_from_values(device.gen3_device(18, 0.75, 0.05, 3).cpu().numpy()))
     assert line["n_gpus"] == 2 and line["config"]["primes"] == want and line["value"] > 0
     assert line["scaling"] == "strong" and line["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [1, 2])
+def test_gpu_emulated_n25_equals_single_gpu(k, pkg):
+    """n = 25 (111.6 GB, the largest state one B200 holds; above every size the
+    CPU reference runs): the 2^k-rank schedule and the single-GPU engine agree
+    on every rank (north_star: 1-GPU and k-GPU runs bit-exact at larger n)."""
+    from paper_2302_10083_b200 import _lib, device
+
+    n = 25
+    vd = device.gen3_device(n, 0.75, 0.05, 3)
+    r, cnt = device.dense_prime_ranks_device(vd, n)
+    want = r.cpu().numpy()
+    del r
+    _lib.load().dqmc_release()
+    torch.cuda.empty_cache()
+    got = S.gpu_sharded_prime_ranks_emulated(vd, n, k)
+    torch.cuda.empty_cache()
+    assert len(got) == cnt and np.array_equal(got, want)
