@@ -253,7 +253,7 @@ def _worker(rank, world, port, n, seed, outdir):
         from oracle import gen as G
 
         k = world.bit_length() - 1
-        plan = S.ShardPlan(n, k)
+        plan = S.ShardPlan(n, k, m=2)  # 3^(k+2) super-blocks keep the CPU oracle calls few
         nl = n - k
         v = G.gen3(n, 0.75, 0.05, seed)
         comm = S.ProcessComm()
