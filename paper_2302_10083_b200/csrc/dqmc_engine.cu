@@ -72,6 +72,10 @@ Plan make_plan(int n, bool padded) {
             for (int c = 0; c < take; c++) p.ib_D[p.m - 2 - q] |= 1u << rest[i++];
         }
     }
+    // zero-skip flags (n = 24: groups 6 + 6, piece-major, one column per C
+    // tile): ~15% of D items and ~18% of E tiles are all zero at config 4
+    // (tools/sparsity.py) and are skipped without touching HBM
+    p.nz = p.pm && p.m == 2 && p.r[1] == kGroupMax && p.ib_C != 0;
     return p;
 }
 
@@ -635,6 +639,7 @@ void dqmc_release(void) {
     cudaFree(g_eng.tt_tmp);
     cudaFree(g_eng.in_tmp);
     cudaFree(g_eng.ranks);
+    cudaFree(g_eng.nzflags);
     for (auto &b : g_eng.free_pinned) cudaFreeHost(b.ptr);
     if (g_eng.stream) cudaStreamDestroy(g_eng.stream);
     if (g_eng.stream2) cudaStreamDestroy(g_eng.stream2);

@@ -432,19 +432,40 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     const int64_t blk0 = tile * NB;  // logical (rank) block
     const int64_t pitch = fa.pitch ? fa.pitch : NB;
     const uint32_t *src = state + tile * pitch * 8;
+    // zero-skip flags (Plan::nz): pass C saw no nonzero cell in this tile
+    auto tile_zero = [&](int64_t t) {
+        const uint32_t t32 = (uint32_t)t, nr = (uint32_t)fa.pm_nr;
+        const uint32_t u = t32 / nr, l = t32 - u * nr;
+        return ((__ldg(&fa.nz_e[l * kNzWords + (u >> 5)]) >> (u & 31)) & 1u) == 0u;
+    };
+    if (fa.nz_e && tile_zero(tile)) {
+        if (threadIdx.x == 0) {
+            fa.tile_base[tile] = 0;
+            fa.tile_cnt[tile] = 0;
+            if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + fa.rank_add;
+        }
+        return;
+    }
     if (threadIdx.x == 0 && fa.pm_nr) {
         // piece-major group 0: the tile is pm_np pieces 3^r pieces apart; boxes
-        // of 256 pieces (map ma) and one remainder box (map mb)
+        // of 256 pieces (map ma) and one remainder box (map mb). Tiles of a
+        // piece-major plan number < 3^12: 32-bit index arithmetic (the 64-bit
+        // division this thread used to do held the other warps at the barrier)
         mbar_init(&mbar, 1);
         mbar_expect_tx(&mbar, fa.pm_np * 128);
         const int nfull = fa.pm_np >> 8, rem = fa.pm_np & 255;
-        const int q1 = (int)(tile % fa.pm_nr), up = (int)(tile / fa.pm_nr);
+        const uint32_t t32 = (uint32_t)tile, nr = (uint32_t)fa.pm_nr;
+        const int up = (int)(t32 / nr), q1 = (int)(t32 - (uint32_t)up * nr);
         for (int j = 0; j < nfull; j++) tma_load_4d(sm + j * 256 * 32, &ma, 0, 256 * j, q1, up, &mbar);
         if (rem) tma_load_4d(sm + nfull * 256 * 32, &mb, 0, 256 * nfull, q1, up, &mbar);
+    } else if (threadIdx.x == 32 && fa.pm_nr) {
+        // warm L2 for the CTA that takes this slot a generation later (issued
+        // by another warp, off the path to the barrier)
         const int pf = (int)blockIdx.x + fa.prefetch;
-        if (fa.prefetch > 0 && pf < (int)gridDim.x) {
-            const int64_t t2 = tile + fa.prefetch;
-            const int q1b = (int)(t2 % fa.pm_nr), upb = (int)(t2 / fa.pm_nr);
+        if (fa.prefetch > 0 && pf < (int)gridDim.x && !(fa.nz_e && tile_zero(tile + fa.prefetch))) {
+            const int nfull = fa.pm_np >> 8, rem = fa.pm_np & 255;
+            const uint32_t t2 = (uint32_t)(tile + fa.prefetch), nr = (uint32_t)fa.pm_nr;
+            const int upb = (int)(t2 / nr), q1b = (int)(t2 - (uint32_t)upb * nr);
             for (int j = 0; j < nfull; j++) tma_prefetch_4d(&ma, 0, 256 * j, q1b, upb);
             if (rem) tma_prefetch_4d(&mb, 0, 256 * nfull, q1b, upb);
         }
@@ -518,6 +539,12 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
     return DQMC_OK;
 }
 
+// E's zero-skip flags: written by pass C of the same fused plan on the engine state
+const uint32_t *nz_e_flags(const Plan &p, const uint32_t *state) {
+    if (!p.nz || state != g_eng.state || !g_eng.nzflags) return nullptr;
+    return g_eng.nzflags + (p.pitch / kRowBlocks) * kNzWords;
+}
+
 // Final stage: E (+ scan + reorder). Source: the truth table (k_small, fused
 // A+E, when tt32 != null) or a merged/reduced state. Returns the prime count.
 }  // namespace
@@ -562,6 +589,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     fa.tile0 = 0;
     fa.pitch = p.pitch;
     fa.prefetch = 3 * g_eng.num_sms;  // one generation of resident CTAs (3 per SM): 9.23 -> 9.0 ms at n=24
+    fa.nz_e = nz_e_flags(p, state);
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
     if (tt32) {
         k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
@@ -682,6 +710,7 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
         fa.tile_cnt = g_eng.tile_cnt;
         fa.prefetch = 3 * g_eng.num_sms;
         fa.pitch = p.pitch;
+        fa.nz_e = nz_e_flags(p, state);
         CUtensorMap ma, mb;
         if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
         CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));

@@ -54,7 +54,10 @@ constexpr int kStridedThreads = 288;  // 9 warps: 27 sub-cube tasks per round di
 constexpr int kTileThreads = 224;   // 7 warps: the 4+3 C0 rounds divide into 1 and 3 tasks/thread
 // pass E: 12 warps x 3 CTAs (smem-limited) = 36 warps/SM to hide LDS/shuffle
 // latency; 56 registers/thread is the most that still fits 3 CTAs.
-constexpr int kFinalThreads = 384;
+#ifndef DQMC_E_THREADS
+#define DQMC_E_THREADS 384
+#endif
+constexpr int kFinalThreads = DQMC_E_THREADS;
 constexpr int kMaxKill = 8;         // parent bitmaps one final pass can clear (sharded path)
 
 enum Mode { MERGE_ONLY = 0, MERGE_REDUCE = 1, REDUCE_ONLY = 2 };
@@ -100,6 +103,7 @@ struct FinalArgs {
     int64_t pitch = 0;          // storage blocks per tile (0: 3^G, the reference layout)
     int pm_nr = 0;              // piece-major group 0 (make_plan): its 3^r rows; 0 = contiguous tiles
     int pm_np = 0;              // pieces (128 B) per tile
+    const uint32_t *nz_e = nullptr;  // zero-tile flags (Plan::nz): bit u of row l = tile (u, l) may be nonzero
 };
 
 // ---------------------------------------------------------------------------
@@ -237,7 +241,10 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
 // a 2-way bank conflict costs MIO wavefronts, which have slack, where a lane
 // half-swap would cost 16 ALU selects per block). Warp-uniform iterations so
 // an all-zero warp can skip (sparse).
-__device__ __forceinline__ void inblock_round(uint32_t *tile, int nblocks, uint32_t ib_mask, int nct, int sparse) {
+// blkmask (optional, shared): bit j of word w = block 32w + j is nonzero after
+// the round (every word written, zero for skipped warps).
+__device__ __forceinline__ void inblock_round(uint32_t *tile, int nblocks, uint32_t ib_mask, int nct, int sparse,
+                                              uint32_t *blkmask = nullptr) {
     const int lane = threadIdx.x & 31;
     for (int t0 = (int)(threadIdx.x & ~31u); t0 < nblocks; t0 += nct) {
         const int t = t0 + lane;
@@ -245,16 +252,32 @@ __device__ __forceinline__ void inblock_round(uint32_t *tile, int nblocks, uint3
         uint4 *p = reinterpret_cast<uint4 *>(tile + (in ? t : 0) * 8);
         uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
         if (in) x0 = p[0], x1 = p[1];
-        if (sparse && !__any_sync(0xffffffffu, (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u)) continue;
+        if (sparse && !__any_sync(0xffffffffu, (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u)) {
+            if (blkmask && lane == 0) blkmask[t0 >> 5] = 0u;
+            continue;
+        }
         uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         inblock_reduce(v, ib_mask);
         if (in) {
             p[0] = make_uint4(v[0], v[1], v[2], v[3]);
             p[1] = make_uint4(v[4], v[5], v[6], v[7]);
         }
+        if (blkmask) {
+            const uint32_t nzb =
+                __ballot_sync(0xffffffffu, in && (v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7]) != 0u);
+            if (lane == 0) blkmask[t0 >> 5] = nzb;
+        }
     }
 }
 
+// 4:1 OR-compaction of a 32-bit block mask: bit k of the result = any of bits 4k..4k+3
+__device__ __forceinline__ uint32_t or4_compact(uint32_t w) {
+    uint32_t m = w | (w >> 1);
+    m = (m | (m >> 2)) & 0x11111111u;
+    m = (m | (m >> 3)) & 0x03030303u;
+    m = (m | (m >> 6)) & 0x000F000Fu;
+    return (m | (m >> 12)) & 0xFFu;
+}
 
 // ---------------------------------------------------------------------------
 // contiguous C0 tile: 3^g blocks x 8 words in shared memory
@@ -310,7 +333,14 @@ struct Plan {
     int64_t pitch = 0;   // storage blocks per C0 tile (3^g, or 3^g rounded up to 128 B)
     uint64_t sbytes = 0; // storage bytes of the state
     bool pm = false;     // piece-major storage of group 0 (see make_plan)
+    bool nz = false;     // pass C records which D items / E tiles can be nonzero (see make_plan)
 };
+
+// Zero-skip flags of the n = 24 plan (Plan::nz): pass C ORs, per item (piece
+// x, group-0 row l), the 729-bit mask of its nonzero rows u into row x of
+// nz_d (D item (x, u)) and row l of nz_e (E tile (u, l)); rows are
+// kNzWords words. REDUCE only clears bits, so a zero flag is exact for D and E.
+constexpr int kNzWords = 24;
 
 Plan make_plan(int n, bool padded = true);
 
@@ -377,6 +407,8 @@ struct Engine {
     int64_t hint_count = 0;           // prime count of the last host call (sizes the pinned output)
     uint32_t *tt_tmp = nullptr;
     size_t tt_tmp_cap = 0;  // bytes
+    uint32_t *nzflags = nullptr;  // Plan::nz flags: nz_d rows then nz_e rows
+    size_t nzflags_cap = 0;       // words
     void *in_tmp = nullptr;
     size_t in_tmp_cap = 0;
     int64_t *ranks = nullptr;

@@ -18,7 +18,8 @@ constexpr int kSparseSkip = 1;
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     k_strided_pipe(const __grid_constant__ CUtensorMap tmap,
-                   int64_t ncol, int64_t nitems, uint32_t ib_mask, int pm, int sparse) {
+                   int64_t ncol, int64_t nitems, uint32_t ib_mask, int pm, int sparse,
+                   const uint32_t *__restrict__ nz_d) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2;
     constexpr int NR = SM::NR;
@@ -39,6 +40,14 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     // time (a contiguous range per CTA measured 16.0 vs 13.9 ms at n = 24)
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     auto item = [&](int64_t i) { return blockIdx.x + i * gridDim.x; };
+    // zero-skip flags (piece-major, Plan::nz): item (x = col, u = outer) is all
+    // zero when pass C saw no nonzero row u in piece x; both roles skip it and
+    // number the remaining items k = 0, 1, ... for the buffers and phases
+    auto zero = [&](int64_t it) {
+        if (!nz_d) return false;
+        const int64_t col = it % ncol, outer = it / ncol;
+        return ((__ldg(&nz_d[col * kNzWords + (outer >> 5)]) >> (outer & 31)) & 1u) == 0u;
+    };
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
@@ -51,40 +60,50 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     if (warp == CW) {
         // ------------------------------ producer warp (one elected lane)
         if (lane == 0) {
-            for (int64_t i = 0; i < L + 2; i++) {
-                const int b = (int)(i & 1);
-                uint32_t *tile = smem + b * SM::TILE_WORDS;
-                const bool st = i >= 2;
-                if (st) {
-                    const int64_t it = item(i - 2);
-                    mbar_wait(&computed[b], (unsigned)(((i - 2) >> 1) & 1));
-                    int c0, c2, c3;
-                    crd(it, c0, c2, c3);
+            int64_t pend0 = -1, pend1 = -1;  // item held in buffer 0 / 1
+            int64_t k = 0;
+            auto store = [&](int64_t kk) {  // the stores of slot kk (buffer kk & 1) once computed
+                const int b = (int)(kk & 1);
+                const uint32_t *tile = smem + b * SM::TILE_WORDS;
+                mbar_wait(&computed[b], (unsigned)((kk >> 1) & 1));
+                int c0, c2, c3;
+                crd(b ? pend1 : pend0, c0, c2, c3);
 #pragma unroll
-                    for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
-                        tma_store_4d(&tmap, c0, x * SM::BOXR, c2, c3, tile + x * SM::BOXR * PITCH);
-                        bulk_commit();
-                    }
+                for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
+                    tma_store_4d(&tmap, c0, x * SM::BOXR, c2, c3, tile + x * SM::BOXR * PITCH);
+                    bulk_commit();
                 }
-                if (i < L) {
-                    const int64_t it = item(i);
-                    int c0, c2, c3;
-                    crd(it, c0, c2, c3);
-                    // each box is reloaded as soon as its store has read it out of
-                    // smem: the next tile's load overlaps the previous tile's store
-                    mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
-                    static_assert(SM::NBOX <= 3, "box-wise store/load overlap handles <= 3 boxes");
+            };
+            for (int64_t i = 0; i < L; i++) {
+                const int64_t it = item(i);
+                if (zero(it)) continue;
+                const int b = (int)(k & 1);
+                uint32_t *tile = smem + b * SM::TILE_WORDS;
+                const bool st = k >= 2;
+                if (st) store(k - 2);
+                int c0, c2, c3;
+                crd(it, c0, c2, c3);
+                // each box is reloaded as soon as its store has read it out of
+                // smem: the next tile's load overlaps the previous tile's store
+                mbar_expect_tx(&full[b], SM::TILE_WORDS * 4);
+                static_assert(SM::NBOX <= 3, "box-wise store/load overlap handles <= 3 boxes");
 #pragma unroll
-                    for (int x = 0; x < SM::NBOX; x++) {
-                        if (st) {
-                            if (SM::NBOX - 1 - x == 2) bulk_wait_read<2>();
-                            else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
-                            else bulk_wait_read<0>();
-                        }
-                        tma_load_4d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, c2, c3, &full[b]);
+                for (int x = 0; x < SM::NBOX; x++) {
+                    if (st) {
+                        if (SM::NBOX - 1 - x == 2) bulk_wait_read<2>();
+                        else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
+                        else bulk_wait_read<0>();
                     }
+                    tma_load_4d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, c2, c3, &full[b]);
                 }
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
+                if (b) pend1 = it;
+                else pend0 = it;
+                k++;
+            }
+            for (int64_t kk = k >= 2 ? k - 2 : 0; kk < k; kk++) {
+                store(kk);
+                bulk_wait_read<0>();
             }
             bulk_wait0();
         }
@@ -93,10 +112,13 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 
     // ---------------------------------- compute warps
     constexpr int NCT = CW * 32;
+    int64_t k = 0;
     for (int64_t i = 0; i < L; i++) {
-        const int b = (int)(i & 1);
+        if (zero(item(i))) continue;
+        const int b = (int)(k & 1);
         const int tb = b * SM::TILE_WORDS;
-        mbar_wait(&full[b], (unsigned)((i >> 1) & 1));
+        mbar_wait(&full[b], (unsigned)((k >> 1) & 1));
+        k++;
         // round 1: reduce the R1 axes
         for (int tt = warp; tt < N2 * CC; tt += CW) {
             const int t2 = tt % N2, h = tt / N2;
@@ -141,7 +163,8 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
-                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse) {
+                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse, uint32_t *__restrict__ nz_d,
+                        uint32_t *__restrict__ nz_e, int nz_nr) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
@@ -149,6 +172,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t stage_full[2], stage_free[2], tile_done[2], tile_free[2];
+    __shared__ uint32_t s_blk[2][4 * kNzWords];  // nonzero blocks of the tile (zero-skip flags, CC = 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
@@ -179,21 +203,38 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
         return;
     }
     if (warp == CW + 1) {  // ------------------------------ store warp
-        if (lane == 0) {
-            for (int64_t i = 0; i < L; i++) {
-                const int b = (int)(i & 1);
-                const int64_t it = blockIdx.x + i * gridDim.x;
-                mbar_wait(&tile_done[b], (unsigned)((i >> 1) & 1));
+        for (int64_t i = 0; i < L; i++) {
+            const int b = (int)(i & 1);
+            const int64_t it = blockIdx.x + i * gridDim.x;
+            mbar_wait(&tile_done[b], (unsigned)((i >> 1) & 1));
+            const int64_t col = it % ncol;
+            if (lane == 0) {
                 const uint32_t *tile = smem + b * SM::TILE_WORDS;
-                const int c0 = (int)((it % ncol) * 32 * CC);
+                const int c0 = (int)(col * 32 * CC);
 #pragma unroll
                 for (int x = 0; x < SM::NBOX; x++) tma_store_3d(&tmap, c0, x * SM::BOXR, 0, tile + x * SM::BOXR * PITCH);
                 bulk_commit();
+            }
+            if (nz_d && lane < kNzWords) {
+                // publish the nonzero rows u (4 blocks each) of item (x, l):
+                // D item (x, u), E tile (u, l)
+                const int nw = (NR * kRowBlocks + 31) / 32;
+                uint32_t w = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (4 * lane + q < nw) w |= or4_compact(s_blk[b][4 * lane + q]) << (8 * q);
+                if (w) {
+                    atomicOr(&nz_d[(col / nz_nr) * kNzWords + lane], w);
+                    atomicOr(&nz_e[(col % nz_nr) * kNzWords + lane], w);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
                 bulk_wait_read0();
                 mbar_arrive(&tile_free[b]);
             }
-            bulk_wait0();
         }
+        if (lane == 0) bulk_wait0();
         return;
     }
 
@@ -254,7 +295,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse);
+            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse, nz_d ? s_blk[b] : nullptr);
         }
         fence_async_smem();
         __syncwarp();
@@ -337,7 +378,8 @@ int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2
 }
 
 template <int R1, int R2, int MODE>
-int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s) {
+int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s,
+                uint32_t *nz) {
     using SM = PipeSmem<R1, R2>;
     constexpr int CC = pipe_cols<R1, R2>();  // 128-B columns per tile
     CUtensorMap map, gmap;
@@ -356,23 +398,24 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
         k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(
-            map, gmap, ncolg, nitems, ib, kSparseSkip);
+            map, gmap, ncolg, nitems, ib, kSparseSkip, nz, nz ? nz + (Q / kRowBlocks / pow3l(R1 + R2)) * kNzWords : nullptr,
+            P3<R1 + R2>::v);
     else
-        k_strided_pipe<R1, R2><<<grid, SM::THREADS, SM::SMEM, s>>>(map, ncolg, nitems, ib, pm ? 1 : 0, kSparseSkip);
+        k_strided_pipe<R1, R2><<<grid, SM::THREADS, SM::SMEM, s>>>(map, ncolg, nitems, ib, pm ? 1 : 0, kSparseSkip, nz);
     CK(cudaGetLastError());
     return DQMC_OK;
 }
 
 template <int MODE>
 int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s,
-                     bool pm = false) {
+                     bool pm = false, uint32_t *nz = nullptr) {
     switch (r) {
-        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s);
-        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s);
+        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
+        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
+        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
+        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
+        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
+        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s, nz);
     }
 }
 
@@ -403,12 +446,21 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
     const uint64_t S = (uint64_t)p.nblocks * 32 * nbatch;
     if (nbatch > 1 && (fused || p.pm)) return set_err(DQMC_ERR_INVALID, "internal: batched reduce is reduce-only");
     int rc;
+    // zero-skip flags (Plan::nz): pass C writes them, pass D and E read them
+    uint32_t *nz = nullptr;
+    size_t nz_words = 0;
+    if (fused && p.nz) {
+        nz_words = (size_t)(p.pitch / kRowBlocks + pow3l(p.r[0])) * kNzWords;
+        if ((rc = grow(g_eng.nzflags, g_eng.nzflags_cap, nz_words, 4))) return rc;
+        nz = g_eng.nzflags;
+    }
     {
         const int k = p.m - 1;
         const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         if (fused) {
-            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s))) return rc;
+            if (nz) CK(cudaMemsetAsync(nz, 0, nz_words * 4, s));
+            if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s, false, nz))) return rc;
             tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(S * std::pow(2.0 / 3.0, p.r[k]) + S));
         } else {
             if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, nbatch, p.ib_C, s))) return rc;
@@ -421,7 +473,7 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
         if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above) * nbatch, p.ib_D[k], s,
-                                                k == 0 && p.pm)))
+                                                k == 0 && p.pm, k == 0 ? nz : nullptr)))
             return rc;
         tm.mark("k_strided<REDUCE>", 2 * S);
     }
