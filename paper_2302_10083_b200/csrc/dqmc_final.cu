@@ -7,6 +7,8 @@
 // tile its rank-order position, and k_reorder moves the ranks there.
 #include <cub/device/device_scan.cuh>
 
+#include <type_traits>
+
 #include "dqmc_internal.cuh"
 
 namespace dqmc {
@@ -53,12 +55,30 @@ __device__ void tile_reduce_c0(uint32_t *sm, int g) {
 // one packed warp scan serves every group: the phases are short latency
 // chains, which is what bounds this pass (3 CTAs/SM, smem-limited).
 template <int NT>
-__device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa) {
-    constexpr int kMaxIter = ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;  // ceil(max warp range / 32)
+__host__ __device__ constexpr int finish_iters() {  // ceil(max warp range / 32)
+    return ((kC0MaxBlocks + NT / 32 - 1) / (NT / 32) + 31) / 32;
+}
+
+// shared scratch of the final stage (one instance per kernel, both paths)
+// (block counts are <= 243; range-relative block indices fit a byte when a
+// warp's range is at most 256 blocks: 3 CTAs of E fit the SM only so)
+template <int NT>
+struct FinishSmem {
+    using Idx = typename std::conditional<(finish_iters<NT>() * 32 <= 256), uint8_t, uint16_t>::type;
+    int64_t warp_off[NT / 32];
+    int64_t tile_off;
+    Idx lst[NT / 32][finish_iters<NT>() * 32];       // nonzero blocks / the emission list
+    uint8_t lcnt[NT / 32][finish_iters<NT>() * 32];  // block popcounts / prime counts of the listed blocks
+};
+
+template <int NT>
+__device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa,
+                                            FinishSmem<NT> &fs) {
+    constexpr int kMaxIter = finish_iters<NT>();
     constexpr int kPk = (kMaxIter + 1) / 2;
-    __shared__ int64_t s_warp_off[NT / 32];
-    __shared__ int64_t s_tile_off;
-    __shared__ uint16_t s_cnt[NT / 32][kMaxIter][32];  // slow-path block popcounts, then the emission list
+    int64_t *s_warp_off = fs.warp_off;
+    int64_t &s_tile_off = fs.tile_off;
+    uint8_t(*s_cnt)[kMaxIter][32] = reinterpret_cast<uint8_t(*)[kMaxIter][32]>(&fs.lcnt[0][0]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int nwarps = NT / 32;  // compile-time: the range split needs no runtime division
     const int b0 = nb * warp / nwarps, b1 = nb * (warp + 1) / nwarps;
@@ -129,7 +149,7 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
                 cj = __popc(x0.x) + __popc(x0.y) + __popc(x0.z) + __popc(x0.w) + __popc(x1.x) + __popc(x1.y) +
                      __popc(x1.z) + __popc(x1.w);
             }
-            s_cnt[warp][j][lane] = (uint16_t)cj;
+            s_cnt[warp][j][lane] = (uint8_t)cj;
         }
         __syncwarp();
 #pragma unroll
@@ -189,14 +209,14 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
     //     busy: reload the block, popcount, one warp scan for the positions,
     //     walk the set bits. Stores of one step ascend with the lane and coalesce.
     const int64_t off = s_tile_off + s_warp_off[warp];
-    uint16_t *lst = &s_cnt[warp][0][0];  // kMaxIter * 32 entries >= the warp's range
+    auto *lst = &fs.lst[warp][0];  // kMaxIter * 32 entries >= the warp's range
     const uint32_t lt = (1u << lane) - 1u;
     int n = 0;
 #pragma unroll
     for (int j = 0; j < kMaxIter; j++) {
         const uint32_t c = (pk[j >> 1] >> (16 * (j & 1))) & 0xffffu;
         const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
-        if (c) lst[n + __popc(m & lt)] = (uint16_t)(32 * j + lane);
+        if (c) lst[n + __popc(m & lt)] = (typename FinishSmem<NT>::Idx)(32 * j + lane);
         n += __popc(m);
     }
     __syncwarp();
@@ -274,6 +294,209 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
             }
         }
     }
+}
+
+// Prime block of a C0 tile as ONE parallel REDUCE step over all G tile axes
+// (+ the in-block axes of ib_mask): P(b) = M(b) & ~(OR over fixed block digits
+// j of M(b + (2 - d_j) 3^j) | in-block kills of M(b)), every kill read from the
+// unmodified input tile (exact: the parallel-step argument of DESIGN.md §3;
+// cube_reduce_par applies the same step to register sub-cubes). A zero block
+// needs no parent: the cost follows the nonzero blocks, not the tile.
+template <int G>
+__device__ __forceinline__ void prime_block(const uint32_t *sm, int b, uint32_t ib_mask, uint32_t (&v)[8]) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+    const uint4 a0 = p[0], a1 = p[1];
+    v[0] = a0.x, v[1] = a0.y, v[2] = a0.z, v[3] = a0.w, v[4] = a1.x, v[5] = a1.y, v[6] = a1.z, v[7] = a1.w;
+    uint4 k0 = make_uint4(0, 0, 0, 0), k1 = k0;
+    int q = b;
+#pragma unroll
+    for (int j = 0; j < G; j++) {
+        const int q3 = q / 3, d = q - 3 * q3;
+        q = q3;
+        if (d != 2) {
+            const uint4 *pp = reinterpret_cast<const uint4 *>(sm + (b + (2 - d) * pow3i(j)) * 8);
+            const uint4 c0 = pp[0], c1 = pp[1];
+            k0 = make_uint4(k0.x | c0.x, k0.y | c0.y, k0.z | c0.z, k0.w | c0.w);
+            k1 = make_uint4(k1.x | c1.x, k1.y | c1.y, k1.z | c1.z, k1.w | c1.w);
+        }
+    }
+    if (ib_mask) inblock_reduce(v, ib_mask);  // kills from the block's own input values
+    v[0] &= ~k0.x, v[1] &= ~k0.y, v[2] &= ~k0.z, v[3] &= ~k0.w;
+    v[4] &= ~k1.x, v[5] &= ~k1.y, v[6] &= ~k1.z, v[7] &= ~k1.w;
+}
+
+// Final stage of one C0 tile whose tile axes are NOT yet reduced (the fused
+// plans). Pass 0: each warp compacts its contiguous block range to the list of
+// its nonzero blocks; the tile's list is their concatenation (rank order).
+// Pass A: the list is cut into batches of 32 entries, batch i to warp
+// i mod NWARP; each lane reduces its block on its own (prime_block) and
+// counts its primes. After the tile's range reservation, pass B emits each
+// batch in rank order (a warp's first batch keeps its primes in registers,
+// later ones are reduced again). The tile in shared memory is only read.
+// Replaces two register-cube rounds over every word of the tile and a
+// popcount pass (round 2b).
+// Returns false (nothing done after pass 0) when the tile has more than
+// kSparseMax nonzero blocks: the register-cube rounds are cheaper there
+// (n = 24, config 4: E 8.22 ms rounds only, 8.07 sparse only, 7.09 with the
+// switch at 600 (7.18 at 400, 7.85 at 300); P(on) = 0.99: 14.7 / 24.5 / 15.3).
+constexpr int kSparseMax = 600;
+
+template <int NT, int G>
+__device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t tile, int64_t blk0,
+                                                   const FinalArgs &fa, FinishSmem<NT> &fs) {
+    constexpr int NB = pow3i(G);
+    constexpr int NWARP = NT / 32;
+    constexpr int kMaxIter = ((NB + NWARP - 1) / NWARP + 31) / 32;
+    constexpr int kMaxBatch = (NB + 31) / 32;
+    static_assert(kMaxIter <= finish_iters<NT>(), "scratch sized for the largest tile");
+    __shared__ int s_off[NWARP + 1];        // nonzero blocks of each warp's range (entry w + 1)
+    __shared__ int s_pre[NWARP];            // their list offsets
+    __shared__ int s_bat[kMaxBatch + 1];    // primes per batch, then their exclusive prefix
+    int64_t &s_tile_off = fs.tile_off;
+    auto &s_lst = fs.lst;    // each warp's nonzero blocks (range-relative)
+    auto &s_lcnt = fs.lcnt;  // their prime counts (<= 243)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
+    const uint32_t lt = (1u << lane) - 1u;
+
+    // pass 0: nonzero blocks of the warp's range, in order. The first 32 of
+    // every range are a density sample: a tile whose sample is dense goes to
+    // the register-cube rounds after one barrier.
+    {
+        const int b0 = NB * warp / NWARP, b1 = NB * (warp + 1) / NWARP;
+        int n = 0;
+#pragma unroll
+        for (int j = 0; j < kMaxIter; j++) {
+            const int b = b0 + 32 * j + lane;
+            bool nz = false;
+            if (b < b1) {
+                const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+                const uint4 x0 = p[h], x1 = p[h ^ 1];
+                nz = (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u;
+            }
+            if (j == 0 && kMaxIter > 1 && __syncthreads_count(nz) > kSparseMax * 32 * NWARP / NB) return false;
+            const uint32_t m = __ballot_sync(0xffffffffu, nz);
+            if (nz) s_lst[warp][n + __popc(m & lt)] = (typename FinishSmem<NT>::Idx)(32 * j + lane);
+            n += __popc(m);
+        }
+        if (lane == 0) s_off[warp + 1] = n;
+    }
+    __syncthreads();
+    int ntot = 0;
+#pragma unroll
+    for (int w = 1; w <= NWARP; w++) ntot += s_off[w];
+    if (ntot > kSparseMax) return false;
+    if (threadIdx.x == 0) {  // list offsets of the warps' ranges (s_off is still being read)
+        int acc = 0;
+        for (int w = 0; w < NWARP; w++) s_pre[w] = acc, acc += s_off[w + 1];
+    }
+    __syncthreads();
+    const int nbat = (ntot + 31) >> 5;
+    // list entry -> (warp range, index): the last w with s_pre[w] <= e
+    auto entry = [&](int e, int &w, int &idx) {
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1)
+            if (lo + step < NWARP && s_pre[lo + step] <= e) lo += step;
+        w = lo;
+        idx = e - s_pre[lo];
+    };
+
+    // pass A: primes per listed block, per batch
+    uint32_t v0[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // the primes of this warp's first batch
+#pragma unroll 1
+    for (int bt = warp; bt < nbat; bt += NWARP) {
+        const int e = 32 * bt + lane;
+        uint32_t v[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        int c = 0;
+        if (e < ntot) {
+            int w, idx;
+            entry(e, w, idx);
+            prime_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa.ib_mask, v);
+#pragma unroll
+            for (int k = 0; k < 8; k++) c += __popc(v[k]);
+            s_lcnt[w][idx] = (uint8_t)c;
+        }
+        if (bt == warp) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) v0[k] = v[k];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_bat[bt] = c;
+    }
+    __syncthreads();
+
+    // reserve this tile's range in the scratch output with one atomic;
+    // k_scan_tiles + k_reorder restore rank order
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int bt = 0; bt < nbat; bt++) {
+            const int c = s_bat[bt];
+            s_bat[bt] = acc;
+            acc += c;
+        }
+        const int64_t base = acc ? (int64_t)atomicAdd(fa.alloc, (unsigned long long)acc) : 0;
+        fa.tile_base[tile] = base;
+        fa.tile_cnt[tile] = (int32_t)acc;
+        if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + fa.rank_add;
+        s_tile_off = base;
+    }
+    __syncthreads();
+    if (fa.out == nullptr && fa.out32 == nullptr) return true;
+
+    // pass B: ordered emission (stores of one step ascend with the lane; a
+    // warp-cooperative variant, one prime per lane found by shuffles + fns,
+    // measured slower: 8.69 vs 8.07 ms)
+#pragma unroll 1
+    for (int bt = warp; bt < nbat; bt += NWARP) {
+        const int e = 32 * bt + lane;
+        int cnt = 0, b = 0;
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = v0[k];
+        if (e < ntot) {
+            int w, idx;
+            entry(e, w, idx);
+            cnt = s_lcnt[w][idx];
+            b = NB * w / NWARP + s_lst[w][idx];
+            if (bt != warp && cnt) prime_block<G>(sm, b, fa.ib_mask, v);
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (!cnt) continue;
+        int64_t pos = s_tile_off + s_bat[bt] + (incl - cnt);
+        const uint32_t lbase = (uint32_t)b * 243u;
+        const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+        if (pos + cnt <= fa.cap) {
+            if (fa.out32) {
+                uint32_t *o = fa.out32 + pos;
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    for (uint32_t x = v[k]; x; x &= x - 1) *o++ = lbase + k * 32 + (__ffs(x) - 1);
+            } else {
+                int64_t *o = fa.out + pos;
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    for (uint32_t x = v[k]; x; x &= x - 1) *o++ = rbase + k * 32 + (__ffs(x) - 1);
+            }
+        } else {  // the output is too small: write what fits (the host grows it and reruns)
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                for (uint32_t x = v[k]; x; x &= x - 1, pos++)
+                    if (pos < fa.cap) {
+                        if (fa.out32)
+                            fa.out32[pos] = lbase + k * 32 + (__ffs(x) - 1);
+                        else
+                            fa.out[pos] = rbase + k * 32 + (__ffs(x) - 1);
+                    }
+        }
+    }
+    return true;
 }
 
 // Exclusive scan of the per-tile counts (one CTA) -> rank-order positions and
@@ -483,8 +706,12 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     }
     __syncthreads();
     mbar_wait(&mbar, 0);
+    __shared__ FinishSmem<kFinalThreads> fs;
+    if (!fa.skip_c0 && !fa.kill_tab && !fa.bitmap_out && !fa.rank_add_tab &&
+        tile_finish_sparse<kFinalThreads, G>(sm, tile, blk0, fa, fs))
+        return;
     if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
-    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa);
+    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa, fs);
 }
 
 // n <= 12: the whole problem is one tile; one CTA does A and E.
@@ -492,7 +719,8 @@ __global__ void __launch_bounds__(kTileThreads) k_small(const uint32_t *__restri
     extern __shared__ __align__(16) uint32_t sm[];
     tile_build(sm, tt32, g, 0);
     tile_reduce_c0(sm, g);
-    tile_finish<kTileThreads>(sm, (int)pow3l(g), 0, 0, fa);
+    __shared__ FinishSmem<kTileThreads> fs;
+    tile_finish<kTileThreads>(sm, (int)pow3l(g), 0, 0, fa, fs);
 }
 
 // E's tensor maps for piece-major group 0: dims {32 words, pieces (3^r x 128 B

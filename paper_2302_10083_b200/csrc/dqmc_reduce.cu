@@ -41,13 +41,13 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     auto item = [&](int64_t i) { return blockIdx.x + i * gridDim.x; };
     // zero-skip flags (piece-major, Plan::nz): item (x = col, u = outer) is all
-    // zero when pass C saw no nonzero row u in piece x; both roles skip it and
-    // number the remaining items k = 0, 1, ... for the buffers and phases
-    auto zero = [&](int64_t it) {
-        if (!nz_d) return false;
-        const int64_t col = it % ncol, outer = it / ncol;
-        return ((__ldg(&nz_d[col * kNzWords + (outer >> 5)]) >> (outer & 31)) & 1u) == 0u;
-    };
+    // zero when pass C saw no nonzero row u in piece x. The producer warp lists
+    // the CTA's other items (in the stage area, unused by this kernel) before
+    // the pipeline starts; the compute warps only need their count.
+    uint16_t *s_list = reinterpret_cast<uint16_t *>(smem + 2 * SM::TILE_WORDS);
+    constexpr int kListCap = 4 * SM::STAGE_WORDS;  // uint16 entries in the two stage buffers
+    __shared__ int s_nitems;
+    const bool listed = nz_d != nullptr && L <= kListCap;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
@@ -55,13 +55,38 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             mbar_init(&computed[b], CW);
         }
     }
+    if (warp == CW) {
+        if (listed) {
+            const uint32_t lt = (1u << lane) - 1u;
+            int n = 0;
+            for (int64_t i0 = 0; i0 < L; i0 += 8 * 32) {
+                uint32_t f[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {  // eight flag loads in flight per lane
+                    const int64_t i = i0 + 32 * q + lane;
+                    const int64_t it = item(i < L ? i : 0);
+                    const int64_t col = it % ncol, outer = it / ncol;
+                    f[q] = i < L ? (__ldg(&nz_d[col * kNzWords + (outer >> 5)]) >> (outer & 31)) & 1u : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t m = __ballot_sync(0xffffffffu, f[q] != 0u);
+                    if (f[q]) s_list[n + __popc(m & lt)] = (uint16_t)(i0 + 32 * q + lane);
+                    n += __popc(m);
+                }
+            }
+            if (lane == 0) s_nitems = n;
+        } else if (lane == 0) {
+            s_nitems = (int)L;
+        }
+    }
     __syncthreads();
+    const int K = s_nitems;
 
     if (warp == CW) {
         // ------------------------------ producer warp (one elected lane)
         if (lane == 0) {
             int64_t pend0 = -1, pend1 = -1;  // item held in buffer 0 / 1
-            int64_t k = 0;
             auto store = [&](int64_t kk) {  // the stores of slot kk (buffer kk & 1) once computed
                 const int b = (int)(kk & 1);
                 const uint32_t *tile = smem + b * SM::TILE_WORDS;
@@ -74,10 +99,9 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                     bulk_commit();
                 }
             };
-            for (int64_t i = 0; i < L; i++) {
-                const int64_t it = item(i);
-                if (zero(it)) continue;
-                const int b = (int)(k & 1);
+            for (int k = 0; k < K; k++) {
+                const int64_t it = item(listed ? (int64_t)s_list[k] : (int64_t)k);
+                const int b = k & 1;
                 uint32_t *tile = smem + b * SM::TILE_WORDS;
                 const bool st = k >= 2;
                 if (st) store(k - 2);
@@ -99,9 +123,8 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
                 if (b) pend1 = it;
                 else pend0 = it;
-                k++;
             }
-            for (int64_t kk = k >= 2 ? k - 2 : 0; kk < k; kk++) {
+            for (int kk = K >= 2 ? K - 2 : 0; kk < K; kk++) {
                 store(kk);
                 bulk_wait_read<0>();
             }
@@ -112,13 +135,10 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 
     // ---------------------------------- compute warps
     constexpr int NCT = CW * 32;
-    int64_t k = 0;
-    for (int64_t i = 0; i < L; i++) {
-        if (zero(item(i))) continue;
-        const int b = (int)(k & 1);
+    for (int k = 0; k < K; k++) {
+        const int b = k & 1;
         const int tb = b * SM::TILE_WORDS;
         mbar_wait(&full[b], (unsigned)((k >> 1) & 1));
-        k++;
         // round 1: reduce the R1 axes
         for (int tt = warp; tt < N2 * CC; tt += CW) {
             const int t2 = tt % N2, h = tt / N2;
@@ -215,24 +235,28 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
                 for (int x = 0; x < SM::NBOX; x++) tma_store_3d(&tmap, c0, x * SM::BOXR, 0, tile + x * SM::BOXR * PITCH);
                 bulk_commit();
             }
+            // the nonzero rows u (4 blocks each) of item (x, l), read before the
+            // buffer is released and published after (flags do not gate it)
+            uint32_t w = 0, od = ~0u, oe = ~0u;
+            uint32_t *fd = nullptr, *fe = nullptr;
             if (nz_d && lane < kNzWords) {
-                // publish the nonzero rows u (4 blocks each) of item (x, l):
-                // D item (x, u), E tile (u, l)
                 const int nw = (NR * kRowBlocks + 31) / 32;
-                uint32_t w = 0;
 #pragma unroll
                 for (int q = 0; q < 4; q++)
                     if (4 * lane + q < nw) w |= or4_compact(s_blk[b][4 * lane + q]) << (8 * q);
-                if (w) {
-                    atomicOr(&nz_d[(col / nz_nr) * kNzWords + lane], w);
-                    atomicOr(&nz_e[(col % nz_nr) * kNzWords + lane], w);
-                }
+                // D item (x, u), E tile (u, l); dense inputs: most bits are
+                // already set, so read first (in flight during the wait below)
+                fd = &nz_d[(col / nz_nr) * kNzWords + lane];
+                fe = &nz_e[(col % nz_nr) * kNzWords + lane];
+                if (w) od = __ldcg(fd), oe = __ldcg(fe);
             }
             __syncwarp();
             if (lane == 0) {
                 bulk_wait_read0();
                 mbar_arrive(&tile_free[b]);
             }
+            if ((od & w) != w) atomicOr(fd, w);
+            if ((oe & w) != w) atomicOr(fe, w);
         }
         if (lane == 0) bulk_wait0();
         return;
