@@ -181,6 +181,7 @@ int run_plan(const Plan &p, const uint32_t *tt32, int64_t *ranks, int64_t cap, i
         if ((rc = run_final_retry(p, nullptr, g_eng.state, p.ib_E, -p.rank_sub, ranks, cap, count_only, fo, &total, tm,
                                   s)))
             return rc;
+        if ((rc = nz_account(p, tm, s))) return rc;
     } else {
         if ((rc = run_final_retry(p, tt32, nullptr, p.ib_E, -p.rank_sub, ranks, cap, count_only, fo, &total, tm, s)))
             return rc;

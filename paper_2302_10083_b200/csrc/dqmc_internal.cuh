@@ -536,6 +536,8 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
 int reduce_set_attrs();
 // nbatch: that many consecutive independent states of this plan (reduce-only)
 int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream_t s, int64_t nbatch = 1);
+// timing mode: bytes of the zero-skip passes D and E as really moved
+int nz_account(const Plan &p, Timer &tm, cudaStream_t s);
 
 // final stage E (dqmc_final.cu)
 int final_set_attrs();

@@ -452,7 +452,45 @@ int set_pipe_attr() {
     return DQMC_OK;
 }
 
+// Timing mode: how many D items / E tiles the zero-skip flags let through
+// (out[0] += set bits of the first nd words, out[1] += of the next ne words)
+__global__ void k_nz_count(const uint32_t *__restrict__ f, int nd, int ne, unsigned long long *out) {
+    unsigned long long a = 0, b = 0;
+    for (int i = threadIdx.x; i < nd + ne; i += blockDim.x) (i < nd ? a : b) += __popc(f[i]);
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], a);
+        atomicAdd(&out[1], b);
+    }
+}
+
 }  // namespace
+
+// Bytes the zero-skip passes really moved (DQMC_FLAG_TIMING): the marks of
+// pass D (group 0) and pass E count only the items / tiles not skipped.
+int nz_account(const Plan &p, Timer &tm, cudaStream_t s) {
+    if (!tm.on || !p.nz || !g_eng.nzflags) return DQMC_OK;
+    const int nd = (int)(p.pitch / kRowBlocks) * kNzWords, ne = (int)pow3l(p.r[0]) * kNzWords;
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(g_eng.total) + 4;
+    CK(cudaMemsetAsync(cnt, 0, 16, s));
+    k_nz_count<<<1, 1024, 0, s>>>(g_eng.nzflags, nd, ne, cnt);
+    CK(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t tile_d = (uint64_t)pow3l(p.r[0]) * 128, tile_e = (uint64_t)p.pitch * 32;
+    int last_d = -1, e = -1;
+    for (size_t i = 0; i < tm.names.size(); i++) {
+        if (tm.names[i] == "k_strided<REDUCE>") last_d = (int)i;
+        if (tm.names[i] == "k_c0_final") e = (int)i;
+    }
+    if (last_d >= 0) tm.bytes[last_d] = 2 * h[0] * tile_d;
+    if (e >= 0) tm.bytes[e] = tm.bytes[e] - (uint64_t)p.nblocks * 32 + h[1] * tile_e;  // the state part of E's bytes
+    return DQMC_OK;
+}
 
 int reduce_set_attrs() {
     int rc;
