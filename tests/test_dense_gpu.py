@@ -228,6 +228,31 @@ class TestFullSize:
         assert c3 == g["primes"] and rsha(r.cpu().numpy())[:16] == g["ranks_sha256_prefix"]
 
 
+    @pytest.mark.parametrize("p_on,p_dc", [(0.99, 0.0), (0.5, 0.1)])
+    def test_n24_zero_skip_vs_reference_layout(self, pkg, p_on, p_dc):
+        """The n=24 plan's zero-skip flags (pass C -> D items / E tiles) and the
+        per-tile sparse/round final stage give the same rank list as the
+        reference-layout plan (no flags, no piece-major group) at the config-5
+        density and at a sparser one."""
+        import ctypes
+
+        import torch
+
+        from paper_2302_10083_b200 import _lib, device
+
+        v = device.gen3_device(24, p_on, p_dc, 4)
+        r1, c1 = device.dense_prime_ranks_device(v, 24)
+        out = torch.empty(c1 + 1024, dtype=torch.int64, device="cuda")
+        cnt = ctypes.c_int64(0)
+        _lib.check(_lib.load().dqmc_primes_device(v.data_ptr(), _lib.IN_U8, 24, out.data_ptr(), out.numel(),
+                                                  ctypes.byref(cnt), _lib.FLAG_KEEP_BITMAP,
+                                                  torch.cuda.current_stream().cuda_stream))
+        assert cnt.value == c1
+        assert bool(out[:c1].eq(r1).all())
+        del out, r1
+        torch.cuda.empty_cache()
+
+
 @pytest.mark.slow
 class TestLargestSingleGpu:
     def test_n25_sampled(self, pkg, oracle_mod, gen_mod):
