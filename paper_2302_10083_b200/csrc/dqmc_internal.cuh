@@ -101,6 +101,8 @@ struct FinalArgs {
     int pm_nr = 0;              // piece-major group 0 (make_plan): its 3^r rows; 0 = contiguous tiles
     int pm_np = 0;              // pieces (128 B) per tile
     const uint32_t *nz_e = nullptr;  // zero-tile flags (Plan::nz): bit u of row l = tile (u, l) may be nonzero
+    int slot = 0;                    // per-tile scratch slot (entries); 0: every tile reserves with an atomic
+    int64_t ovf0 = 0;                // first entry of the overflow pool (after the slots)
 };
 
 // ---------------------------------------------------------------------------
