@@ -360,6 +360,24 @@ class TestJobStream:
         for g, w in zip(got, want):
             assert np.array_equal(g, w)
 
+    def test_stream_n24_zero_skip_plan(self, pkg, golden):
+        """The job stream at n = 24 (zero-skip flags, per-tile scratch slots,
+        async count publication): config 4 twice, then the config-5 density (whose
+        tiles overflow their slots), then config 4 again, each equal to the
+        synchronous engine."""
+        from paper_2302_10083_b200 import device
+
+        g = golden["configs"]["4"]
+        v4 = device.gen3_device(24, 0.75, 0.05, 3).cpu().numpy()
+        v5 = device.gen3_device(24, 0.99, 0.0, 4)
+        r5, c5 = device.dense_prime_ranks_device(v5, 24)
+        h5 = rsha(r5.cpu().numpy())
+        del r5
+        got = list(pkg.stream_prime_ranks([v4, v4, v5.cpu().numpy(), v4]))
+        for i in (0, 1, 3):
+            assert len(got[i]) == g["primes"] and rsha(got[i])[:16] == g["ranks_sha256_prefix"]
+        assert len(got[2]) == c5 and rsha(got[2]) == h5
+
     def test_truth_tables_and_repeat(self, pkg, gen_mod):
         t = pkg.TruthTable(17, gen_mod.random_words(17, 0.6, 9))
         want = pkg.dense_prime_ranks(t)
