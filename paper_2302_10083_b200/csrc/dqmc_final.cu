@@ -2,9 +2,15 @@
 // compaction (extract_ranks, dense.py:376-397).
 //
 // Rank order is memory order in the reference layout (block a, bit b = rank
-// a*243 + b), so compaction needs no sort: each tile reserves a range of a
-// scratch buffer with one atomic, a scan of the per-tile counts gives every
-// tile its rank-order position, and k_reorder moves the ranks there.
+// a*243 + b), so compaction needs no sort: each tile writes its primes to a
+// scratch range (its own fixed slot in the n = 24 plan, else a range reserved
+// with one atomic), a scan of the per-tile counts gives every tile its
+// rank-order position, and k_reorder moves the ranks there.
+//
+// A tile is finished one of two ways: sparse tiles reduce each
+// nonzero block on its own as one parallel REDUCE step from the unmodified
+// tile (tile_finish_sparse / prime_block); dense tiles go through register
+// sub-cube rounds over every word (tile_reduce_c0_t) and tile_finish.
 #include <cub/device/device_scan.cuh>
 
 #include <type_traits>

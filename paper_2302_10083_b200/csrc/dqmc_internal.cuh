@@ -19,8 +19,10 @@
 //   pass D  k_strided_pipe       (dqmc_reduce.cu) REDUCE of the other groups +
 //                                 in-block axes; TMA tiles, one producer warp.
 //   pass E  k_c0_final           (dqmc_final.cu)  REDUCE of the C0 axes,
-//                                 popcounts, per-tile scratch reservation and
+//                                 popcounts, per-tile scratch range and
 //                                 ordered compaction; then a scan + k_reorder.
+// The n = 24 plan (Plan::nz) adds zero-skip flags: pass C records which D
+// items and E tiles can be nonzero, D and E skip the others.
 // Small n (<= 12): one CTA does A+E on a single smem tile (k_small).
 // dqmc_engine.cu holds the plan, the workspace and the C ABI; dqmc_input.cu
 // the input conversion and generators; dqmc_shard.cu the sharded path's
