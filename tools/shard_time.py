@@ -1,6 +1,6 @@
 """Time the sharded schedule with all 2^k ranks emulated on one GPU (one
 process, EmulatedComm): ms per call for n and k, against the single-GPU call.
-Usage: python tools/shard_time.py [n] [reps]"""
+Usage: python tools/shard_time.py [n] [reps] [libdqmc variant .so]"""
 import json
 import os
 import sys
@@ -9,7 +9,10 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2302_10083_b200 import device  # noqa: E402
+from paper_2302_10083_b200 import _lib, device  # noqa: E402
+
+if len(sys.argv) > 3:  # a tools/build_variant.py build instead of the in-tree library
+    _lib.LIB_PATH = os.path.abspath(sys.argv[3])
 from paper_2302_10083_b200 import sharded as S  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 24
