@@ -142,14 +142,16 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
                     // only under a nonzero block (~15% at config 4: a zero block
                     // stays zero, so most parent reads are skipped)
                     uint4 k0 = make_uint4(0, 0, 0, 0), k1 = k0;
-#pragma unroll 1
-                    for (int q = 0; q < kMaxKill && kills[q]; q++) {
-                        const uint4 *kq =
-                            reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(kills[q]) +
-                                                            (blk0 + b - slot_blk0) * 8);
-                        const uint4 a0 = kq[0], a1 = kq[1];
-                        k0 = make_uint4(k0.x | a0.x, k0.y | a0.y, k0.z | a0.z, k0.w | a0.w);
-                        k1 = make_uint4(k1.x | a1.x, k1.y | a1.y, k1.z | a1.z, k1.w | a1.w);
+#pragma unroll
+                    for (int q = 0; q < kMaxKill; q++) {  // unrolled: every parent's load in flight at once
+                        const uint64_t kp = __ldg(&kills[q]);
+                        if (kp) {
+                            const uint4 *kq = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(kp) +
+                                                                              (blk0 + b - slot_blk0) * 8);
+                            const uint4 a0 = kq[0], a1 = kq[1];
+                            k0 = make_uint4(k0.x | a0.x, k0.y | a0.y, k0.z | a0.z, k0.w | a0.w);
+                            k1 = make_uint4(k1.x | a1.x, k1.y | a1.y, k1.z | a1.z, k1.w | a1.w);
+                        }
                     }
                     x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
                     x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
@@ -342,6 +344,38 @@ __device__ __forceinline__ void prime_block(const uint32_t *sm, int b, uint32_t 
     v[4] &= ~k1.x, v[5] &= ~k1.y, v[6] &= ~k1.z, v[7] &= ~k1.w;
 }
 
+// The sparse finish's per-block step in general: the C0 step of prime_block
+// (or, skip_c0, the block as it is: the sharded path's reduce_low did the C0
+// axes), then the top-axis kills of the sharded path: the OR of up to
+// kMaxKill parent super-blocks at the block's offset (local or NVLink peer
+// memory), all loads in flight at once.
+template <int G>
+__device__ __forceinline__ void finish_block(const uint32_t *sm, int b, const FinalArgs &fa, const uint64_t *kills,
+                                             int64_t kofs, uint32_t (&v)[8]) {
+    if (fa.skip_c0) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+        const uint4 a0 = p[0], a1 = p[1];
+        v[0] = a0.x, v[1] = a0.y, v[2] = a0.z, v[3] = a0.w, v[4] = a1.x, v[5] = a1.y, v[6] = a1.z, v[7] = a1.w;
+        if (fa.ib_mask) inblock_reduce(v, fa.ib_mask);
+    } else {
+        prime_block<G>(sm, b, fa.ib_mask, v);
+    }
+    if (!kills) return;
+    uint4 k0 = make_uint4(0, 0, 0, 0), k1 = k0;
+#pragma unroll
+    for (int q = 0; q < kMaxKill; q++) {
+        const uint64_t kp = __ldg(&kills[q]);
+        if (kp) {
+            const uint4 *kq = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(kp) + (kofs + b) * 8);
+            const uint4 a0 = kq[0], a1 = kq[1];
+            k0 = make_uint4(k0.x | a0.x, k0.y | a0.y, k0.z | a0.z, k0.w | a0.w);
+            k1 = make_uint4(k1.x | a1.x, k1.y | a1.y, k1.z | a1.z, k1.w | a1.w);
+        }
+    }
+    v[0] &= ~k0.x, v[1] &= ~k0.y, v[2] &= ~k0.z, v[3] &= ~k0.w;
+    v[4] &= ~k1.x, v[5] &= ~k1.y, v[6] &= ~k1.z, v[7] &= ~k1.w;
+}
+
 // Final stage of one C0 tile whose tile axes are NOT yet reduced (the fused
 // plans). Pass 0: each warp compacts its contiguous block range to the list of
 // its nonzero blocks; the tile's list is their concatenation (rank order).
@@ -358,7 +392,7 @@ __device__ __forceinline__ void prime_block(const uint32_t *sm, int b, uint32_t 
 // switch at 600 (7.18 at 400, 7.85 at 300); P(on) = 0.99: 14.7 / 24.5 / 15.3).
 constexpr int kSparseMax = 600;
 
-template <int NT, int G>
+template <int NT, int G, bool SHARD>
 __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t tile, int64_t blk0,
                                                    const FinalArgs &fa, FinishSmem<NT> &fs) {
     constexpr int NB = pow3i(G);
@@ -375,6 +409,13 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
     const uint32_t lt = (1u << lane) - 1u;
+    // SHARD (the sharded extract): this tile's super-block (slot), its parents
+    // and rank offset; the fused plans compile none of it
+    const int64_t slot = SHARD && (fa.kill_tab || fa.rank_add_tab) ? tile / fa.tiles_per_slot : 0;
+    const int64_t slot_blk0 = slot * fa.tiles_per_slot * NB;  // first block of the slot
+    const int64_t rank_add = SHARD && fa.rank_add_tab ? fa.rank_add_tab[slot] - slot_blk0 * 243 : fa.rank_add;
+    const uint64_t *kills = SHARD && fa.kill_tab ? fa.kill_tab + slot * kMaxKill : nullptr;
+    const int64_t kofs = blk0 - slot_blk0;  // the tile's first block within its super-block
 
     // pass 0: nonzero blocks of the warp's range, in order. The first 32 of
     // every range are a density sample: a tile whose sample is dense goes to
@@ -429,7 +470,10 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
         if (e < ntot) {
             int w, idx;
             entry(e, w, idx);
-            prime_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa.ib_mask, v);
+            if (SHARD)
+                finish_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa, kills, kofs, v);
+            else
+                prime_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa.ib_mask, v);
 #pragma unroll
             for (int k = 0; k < 8; k++) c += __popc(v[k]);
             s_lcnt[w][idx] = (uint8_t)c;
@@ -456,7 +500,7 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
         const int64_t base = tile_range(fa, tile, acc);
         fa.tile_base[tile] = base;
         fa.tile_cnt[tile] = (int32_t)acc;
-        if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + fa.rank_add;
+        if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + rank_add;
         s_tile_off = base;
     }
     __syncthreads();
@@ -477,7 +521,12 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
             entry(e, w, idx);
             cnt = s_lcnt[w][idx];
             b = NB * w / NWARP + s_lst[w][idx];
-            if (bt != warp && cnt) prime_block<G>(sm, b, fa.ib_mask, v);
+            if (bt != warp && cnt) {
+                if (SHARD)
+                    finish_block<G>(sm, b, fa, kills, kofs, v);
+                else
+                    prime_block<G>(sm, b, fa.ib_mask, v);
+            }
         }
         int incl = cnt;
 #pragma unroll
@@ -488,7 +537,7 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
         if (!cnt) continue;
         int64_t pos = s_tile_off + s_bat[bt] + (incl - cnt);
         const uint32_t lbase = (uint32_t)b * 243u;
-        const int64_t rbase = (blk0 + b) * 243 + fa.rank_add;
+        const int64_t rbase = (blk0 + b) * 243 + rank_add;
         if (pos + cnt <= fa.cap) {
             if (fa.out32) {
                 uint32_t *o = fa.out32 + pos;
@@ -726,9 +775,13 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     __syncthreads();
     mbar_wait(&mbar, 0);
     __shared__ FinishSmem<kFinalThreads> fs;
-    if (!fa.skip_c0 && !fa.kill_tab && !fa.bitmap_out && !fa.rank_add_tab &&
-        tile_finish_sparse<kFinalThreads, G>(sm, tile, blk0, fa, fs))
-        return;
+    if (!fa.bitmap_out) {
+        if (fa.kill_tab || fa.skip_c0 || fa.rank_add_tab) {
+            if (tile_finish_sparse<kFinalThreads, G, true>(sm, tile, blk0, fa, fs)) return;
+        } else if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs)) {
+            return;
+        }
+    }
     if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
     tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa, fs);
 }
