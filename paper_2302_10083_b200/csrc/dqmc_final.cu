@@ -847,7 +847,7 @@ int64_t tile_slot(const Plan &p) { return p.nz ? 1024 : 0; }
 // E's zero-skip flags: written by pass C of the same fused plan on the engine state
 const uint32_t *nz_e_flags(const Plan &p, const uint32_t *state) {
     if (!p.nz || state != g_eng.state || !g_eng.nzflags) return nullptr;
-    return g_eng.nzflags + (p.pitch / kRowBlocks) * kNzWords;
+    return g_eng.nzflags + nz_e_offset((size_t)(p.pitch / kRowBlocks));
 }
 
 // Final stage: E (+ scan + reorder). Source: the truth table (k_small, fused

@@ -338,10 +338,17 @@ struct Plan {
 };
 
 // Zero-skip flags of the n = 24 plan (Plan::nz): pass C ORs, per item (piece
-// x, group-0 row l), the 729-bit mask of its nonzero rows u into row x of
-// nz_d (D item (x, u)) and row l of nz_e (E tile (u, l)); rows are
-// kNzWords words. REDUCE only clears bits, so a zero flag is exact for D and E.
+// x, group-0 row l), the 729-bit mask of its nonzero rows u into row (x, l/243)
+// of nz_b (box l/243 of D item (x, u)) and row l of nz_e (E tile (u, l)); rows
+// are kNzWords words. REDUCE only clears bits, so a zero flag is exact for D
+// and E.
 constexpr int kNzWords = 24;
+// Flag layout in g_eng.nzflags (npiece = pieces per C0 tile, nr = 3^6 group-0
+// rows): nz_b [npiece][3 boxes of 243 rows][kNzWords] (pass D's items (x, u)
+// per box), nz_e [nr][kNzWords] (pass E's tiles (u, l)), then a zero page of
+// one 243-row box (128-B aligned) that pass D loads its all-zero boxes from.
+inline size_t nz_e_offset(size_t npiece) { return npiece * 3 * kNzWords; }
+inline size_t nz_zero_page(size_t npiece, size_t nr) { return ((npiece * 3 + nr) * kNzWords + 31) & ~(size_t)31; }
 
 Plan make_plan(int n, bool padded = true);
 

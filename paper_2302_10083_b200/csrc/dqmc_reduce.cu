@@ -17,9 +17,9 @@ constexpr int kSparseSkip = 1;
 
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
-    k_strided_pipe(const __grid_constant__ CUtensorMap tmap,
+    k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
                    int64_t ncol, int64_t nitems, uint32_t ib_mask, int pm, int sparse,
-                   const uint32_t *__restrict__ nz_d) {
+                   const uint32_t *__restrict__ nz_b) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2;
     constexpr int NR = SM::NR;
@@ -40,14 +40,17 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     // time (a contiguous range per CTA measured 16.0 vs 13.9 ms at n = 24)
     const int64_t L = nitems > blockIdx.x ? (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     auto item = [&](int64_t i) { return blockIdx.x + i * gridDim.x; };
-    // zero-skip flags (piece-major, Plan::nz): item (x = col, u = outer) is all
-    // zero when pass C saw no nonzero row u in piece x. The producer warp lists
-    // the CTA's other items (in the stage area, unused by this kernel) before
-    // the pipeline starts; the compute warps only need their count.
+    // zero-skip flags (piece-major, Plan::nz): box j (rows 243 j .. 243 j + 242)
+    // of item (x = col, u = outer) is all zero when pass C saw no nonzero row u
+    // in the items (x, l) of those rows. The producer warp lists the CTA's
+    // items with a nonzero box, and their box masks, before the pipeline starts
+    // (in the stage area, unused by this kernel); zero boxes are loaded from a
+    // zero page (L2) and not stored back. The compute warps only need the count.
+    constexpr int kListCap = 2 * SM::STAGE_WORDS;  // uint16 entries, then as many uint8 box masks
     uint16_t *s_list = reinterpret_cast<uint16_t *>(smem + 2 * SM::TILE_WORDS);
-    constexpr int kListCap = 4 * SM::STAGE_WORDS;  // uint16 entries in the two stage buffers
+    uint8_t *s_bm = reinterpret_cast<uint8_t *>(s_list + kListCap);
     __shared__ int s_nitems;
-    const bool listed = nz_d != nullptr && L <= kListCap;
+    const bool listed = nz_b != nullptr && L <= kListCap && SM::NBOX == 3;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; b++) {
@@ -62,16 +65,24 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
             for (int64_t i0 = 0; i0 < L; i0 += 8 * 32) {
                 uint32_t f[8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) {  // eight flag loads in flight per lane
+                for (int q = 0; q < 8; q++) {  // 24 flag loads in flight per lane
                     const int64_t i = i0 + 32 * q + lane;
                     const int64_t it = item(i < L ? i : 0);
                     const int64_t col = it % ncol, outer = it / ncol;
-                    f[q] = i < L ? (__ldg(&nz_d[col * kNzWords + (outer >> 5)]) >> (outer & 31)) & 1u : 0u;
+                    f[q] = 0u;
+#pragma unroll
+                    for (int j = 0; j < 3; j++)
+                        f[q] |= ((__ldg(&nz_b[(col * 3 + j) * kNzWords + (outer >> 5)]) >> (outer & 31)) & 1u) << j;
+                    if (i >= L) f[q] = 0u;
                 }
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const uint32_t m = __ballot_sync(0xffffffffu, f[q] != 0u);
-                    if (f[q]) s_list[n + __popc(m & lt)] = (uint16_t)(i0 + 32 * q + lane);
+                    if (f[q]) {
+                        const int e = n + __popc(m & lt);
+                        s_list[e] = (uint16_t)(i0 + 32 * q + lane);
+                        s_bm[e] = (uint8_t)f[q];
+                    }
                     n += __popc(m);
                 }
             }
@@ -87,20 +98,23 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
         // ------------------------------ producer warp (one elected lane)
         if (lane == 0) {
             int64_t pend0 = -1, pend1 = -1;  // item held in buffer 0 / 1
+            uint32_t bm0 = 7, bm1 = 7;       // its nonzero boxes
             auto store = [&](int64_t kk) {  // the stores of slot kk (buffer kk & 1) once computed
                 const int b = (int)(kk & 1);
                 const uint32_t *tile = smem + b * SM::TILE_WORDS;
                 mbar_wait(&computed[b], (unsigned)((kk >> 1) & 1));
                 int c0, c2, c3;
                 crd(b ? pend1 : pend0, c0, c2, c3);
+                const uint32_t bm = b ? bm1 : bm0;
 #pragma unroll
-                for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box
-                    tma_store_4d(&tmap, c0, x * SM::BOXR, c2, c3, tile + x * SM::BOXR * PITCH);
+                for (int x = 0; x < SM::NBOX; x++) {  // one bulk group per box (empty for a zero box)
+                    if ((bm >> x) & 1u) tma_store_4d(&tmap, c0, x * SM::BOXR, c2, c3, tile + x * SM::BOXR * PITCH);
                     bulk_commit();
                 }
             };
             for (int k = 0; k < K; k++) {
                 const int64_t it = item(listed ? (int64_t)s_list[k] : (int64_t)k);
+                const uint32_t bm = listed ? s_bm[k] : 7u;
                 const int b = k & 1;
                 uint32_t *tile = smem + b * SM::TILE_WORDS;
                 const bool st = k >= 2;
@@ -118,11 +132,14 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
                         else if (SM::NBOX - 1 - x == 1) bulk_wait_read<1>();
                         else bulk_wait_read<0>();
                     }
-                    tma_load_4d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, c2, c3, &full[b]);
+                    if ((bm >> x) & 1u)
+                        tma_load_4d(tile + x * SM::BOXR * PITCH, &tmap, c0, x * SM::BOXR, c2, c3, &full[b]);
+                    else  // all-zero box: zeros from the L2-resident zero page, no HBM read
+                        tma_load_4d(tile + x * SM::BOXR * PITCH, &zmap, 0, 0, 0, 0, &full[b]);
                 }
                 if (st) bulk_wait_read<0>();  // buffer b is rewritten by compute only after `full`
-                if (b) pend1 = it;
-                else pend0 = it;
+                if (b) pend1 = it, bm1 = bm;
+                else pend0 = it, bm0 = bm;
             }
             for (int kk = K >= 2 ? K - 2 : 0; kk < K; kk++) {
                 store(kk);
@@ -183,7 +200,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
 template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
-                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse, uint32_t *__restrict__ nz_d,
+                        int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse, uint32_t *__restrict__ nz_b,
                         uint32_t *__restrict__ nz_e, int nz_nr) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
@@ -239,14 +256,14 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // buffer is released and published after (flags do not gate it)
             uint32_t w = 0, od = ~0u, oe = ~0u;
             uint32_t *fd = nullptr, *fe = nullptr;
-            if (nz_d && lane < kNzWords) {
+            if (nz_b && lane < kNzWords) {
                 const int nw = (NR * kRowBlocks + 31) / 32;
 #pragma unroll
                 for (int q = 0; q < 4; q++)
                     if (4 * lane + q < nw) w |= or4_compact(s_blk[b][4 * lane + q]) << (8 * q);
                 // D item (x, u), E tile (u, l); dense inputs: most bits are
                 // already set, so read first (in flight during the wait below)
-                fd = &nz_d[(col / nz_nr) * kNzWords + lane];
+                fd = &nz_b[((col / nz_nr) * 3 + (col % nz_nr) / (nz_nr / 3)) * kNzWords + lane];
                 fe = &nz_e[(col % nz_nr) * kNzWords + lane];
                 if (w) od = __ldcg(fd), oe = __ldcg(fe);
             }
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             // thread per block; plain LDS.128 pairs (a 2-way bank conflict costs
             // MIO wavefronts, which have slack here; a lane half-swap would cost
             // 16 ALU selects per block on the saturated ALU pipe)
-            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse, nz_d ? s_blk[b] : nullptr);
+            inblock_round(&smem[tb], NR * kRowBlocks * CC, ib_mask, NCT, sparse, nz_b ? s_blk[b] : nullptr);
         }
         fence_async_smem();
         __syncwarp();
@@ -422,10 +439,26 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     const int grid = (int)std::min<int64_t>(nitems, g_eng.num_sms);
     if (MODE == MERGE_REDUCE)
         k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(
-            map, gmap, ncolg, nitems, ib, kSparseSkip, nz, nz ? nz + (Q / kRowBlocks / pow3l(R1 + R2)) * kNzWords : nullptr,
+            map, gmap, ncolg, nitems, ib, kSparseSkip, nz, nz ? nz + nz_e_offset(Q / kRowBlocks / pow3l(R1 + R2)) : nullptr,
             P3<R1 + R2>::v);
     else
-        k_strided_pipe<R1, R2><<<grid, SM::THREADS, SM::SMEM, s>>>(map, ncolg, nitems, ib, pm ? 1 : 0, kSparseSkip, nz);
+    {
+        CUtensorMap zmap;  // zero-skip mode: the zero page, box {32, BOXR} (a fully-specified map otherwise unused)
+        memset(&zmap, 0, sizeof zmap);
+        if (nz) {
+            if ((rc = ensure_encode())) return rc;
+            const uint32_t *zp = nz + nz_zero_page((size_t)ncolg, (size_t)SM::NR);
+            cuuint64_t dims[4] = {32, (cuuint64_t)SM::BOXR, 1, 1};
+            cuuint64_t strides[3] = {128, (cuuint64_t)SM::BOXR * 128, (cuuint64_t)SM::BOXR * 128};
+            cuuint32_t box[4] = {32, (cuuint32_t)SM::BOXR, 1, 1}, es[4] = {1, 1, 1, 1};
+            CUresult r = g_eng.encode(&zmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (void *)zp, dims, strides, box, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (zero page) failed: " + std::to_string((int)r));
+        }
+        k_strided_pipe<R1, R2><<<grid, SM::THREADS, SM::SMEM, s>>>(map, zmap, ncolg, nitems, ib, pm ? 1 : 0,
+                                                                   kSparseSkip, nz);
+    }
     CK(cudaGetLastError());
     return DQMC_OK;
 }
@@ -473,7 +506,8 @@ __global__ void k_nz_count(const uint32_t *__restrict__ f, int nd, int ne, unsig
 // pass D (group 0) and pass E count only the items / tiles not skipped.
 int nz_account(const Plan &p, Timer &tm, cudaStream_t s) {
     if (!tm.on || !p.nz || !g_eng.nzflags) return DQMC_OK;
-    const int nd = (int)(p.pitch / kRowBlocks) * kNzWords, ne = (int)pow3l(p.r[0]) * kNzWords;
+    const int npiece = (int)(p.pitch / kRowBlocks), nr = (int)pow3l(p.r[0]);
+    const int nd = npiece * 3 * kNzWords, ne = nr * kNzWords;
     unsigned long long *cnt = reinterpret_cast<unsigned long long *>(g_eng.total) + 4;
     CK(cudaMemsetAsync(cnt, 0, 16, s));
     k_nz_count<<<1, 1024, 0, s>>>(g_eng.nzflags, nd, ne, cnt);
@@ -481,13 +515,13 @@ int nz_account(const Plan &p, Timer &tm, cudaStream_t s) {
     unsigned long long h[2] = {0, 0};
     CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const uint64_t tile_d = (uint64_t)pow3l(p.r[0]) * 128, tile_e = (uint64_t)p.pitch * 32;
+    const uint64_t box_d = (uint64_t)(nr / 3) * 128, tile_e = (uint64_t)p.pitch * 32;
     int last_d = -1, e = -1;
     for (size_t i = 0; i < tm.names.size(); i++) {
         if (tm.names[i] == "k_strided<REDUCE>") last_d = (int)i;
         if (tm.names[i] == "k_c0_final") e = (int)i;
     }
-    if (last_d >= 0) tm.bytes[last_d] = 2 * h[0] * tile_d;
+    if (last_d >= 0) tm.bytes[last_d] = 2 * h[0] * box_d;  // the nonzero boxes, read and written
     if (e >= 0) tm.bytes[e] = tm.bytes[e] - (uint64_t)p.nblocks * 32 + h[1] * tile_e;  // the state part of E's bytes
     return DQMC_OK;
 }
@@ -512,9 +546,12 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
     uint32_t *nz = nullptr;
     size_t nz_words = 0;
     if (fused && p.nz) {
-        nz_words = (size_t)(p.pitch / kRowBlocks + pow3l(p.r[0])) * kNzWords;
-        if ((rc = grow(g_eng.nzflags, g_eng.nzflags_cap, nz_words, 4))) return rc;
+        const size_t npiece = (size_t)(p.pitch / kRowBlocks), nr = (size_t)pow3l(p.r[0]);
+        nz_words = (npiece * 3 + nr) * kNzWords;  // nz_b, nz_e: zeroed per call
+        const size_t zp = nz_zero_page(npiece, nr), zwords = (nr / 3) * 32;
+        if ((rc = grow(g_eng.nzflags, g_eng.nzflags_cap, zp + zwords, 4))) return rc;
         nz = g_eng.nzflags;
+        CK(cudaMemsetAsync(nz + zp, 0, zwords * 4, s));
     }
     {
         const int k = p.m - 1;
