@@ -627,7 +627,12 @@ def run_engine_bench(args):
             "unit": UNIT,
             "ms_per_step": t_e2e * 1e3,
             "h2d_bytes_per_step": int(1 << n),
-            "d2h_bytes_per_step": int(cnt * 8 + 8),
+            # results of 4M+ ranks cross PCIe packed: 4-byte tile offsets + the tiles' int64
+            # positions (3^(n-12) tiles) + the count; the host threads widen them to int64 ranks
+            "d2h_bytes_per_step": int(cnt * 4 + 3 ** max(0, n - 12) * 8 + 8) if cnt >= (1 << 22) else int(cnt * 8 + 8),
+            "result_bytes_per_step": int(cnt * 8),
+            "transfer": "packed (uint32 tile offsets over PCIe, widened to int64 ranks by the library's host "
+                        "thread pool inside the timed region)" if cnt >= (1 << 22) else "int64 ranks",
             "api": "paper_2302_10083_b200.stream_prime_ranks (C ABI dqmc_submit_u8 / dqmc_collect), "
                    "three calls in flight, pinned input",
             "calls": n_stream,

@@ -46,7 +46,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DQMC_ABI_VERSION 3
+#define DQMC_ABI_VERSION 4
 
 /* status codes */
 #define DQMC_OK 0
@@ -107,6 +107,19 @@ void dqmc_free_result(dqmc_result_t *res);
 int dqmc_submit_tt(const uint64_t *tt_words, int n, uint32_t flags, int64_t *job);
 int dqmc_submit_u8(const uint8_t *values, int n, uint32_t flags, int64_t *job);
 int dqmc_collect(int64_t job, dqmc_result_t *out);
+
+/* Results of 4M+ ranks leave the device packed (4-byte cell offsets inside
+ * each 3^12-cell tile, rank order: half the PCIe bytes of the reference's
+ * int64 ranks, dense.py:376-397) and are widened to int64 by a pool of host
+ * threads while the next chunk is on the wire. Sets the pool size (0 =
+ * default: min(hardware threads, 16)); returns the previous setting. */
+int dqmc_host_threads(int n);
+/* The widening step itself, host only (no device needed; also what the CPU
+ * tests call): out[i] = (t * tile_cells + rank_add) + off32[i] for tiles
+ * t in [t0, t1) and add + pos[t - t0] <= i < add + pos[t - t0 + 1] (the last
+ * tile ends at `end`). */
+void dqmc_widen_host(const uint32_t *off32, int64_t *out, const int64_t *pos, int64_t add, int64_t end,
+                     int64_t t0, int64_t t1, int64_t tile_cells, int64_t rank_add);
 
 /* Same computation with DEVICE-resident input and output (bench `value`,
  * torch integration). ranks_dev may be NULL (count only). If the count

@@ -47,6 +47,8 @@ EXPORTS = (
     "dqmc_submit_tt",
     "dqmc_submit_u8",
     "dqmc_collect",
+    "dqmc_host_threads",
+    "dqmc_widen_host",
     "dqmc_primes_device",
     "dqmc_last_timings",
     "dqmc_last_pass_bytes",
@@ -135,6 +137,8 @@ def load() -> ctypes.CDLL:
             "dqmc_submit_tt": (i32, [vp, i32, u32, ctypes.POINTER(ctypes.c_int64)]),
             "dqmc_submit_u8": (i32, [vp, i32, u32, ctypes.POINTER(ctypes.c_int64)]),
             "dqmc_collect": (i32, [ctypes.c_int64, ctypes.POINTER(DqmcResult)]),
+            "dqmc_host_threads": (i32, [i32]),
+            "dqmc_widen_host": (None, [vp, vp, vp, i64, i64, i64, i64, i64, i64]),
             "dqmc_primes_device": (i32, [vp, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64), u32, vp]),
             "dqmc_last_timings": (i32, [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), i32]),
             "dqmc_last_pass_bytes": (i32, [ctypes.POINTER(ctypes.c_uint64), i32]),

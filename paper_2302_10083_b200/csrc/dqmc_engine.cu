@@ -94,6 +94,7 @@ int ensure_device() {
     CK(cudaMalloc(&g_eng.alloc, 256));
     CK(cudaStreamCreateWithFlags(&g_eng.stream2, cudaStreamNonBlocking));
     for (int i = 0; i < 16; i++) CK(cudaEventCreateWithFlags(&g_eng.chunk_ev[i], cudaEventDisableTiming));
+    for (int i = 0; i < 16; i++) CK(cudaEventCreateWithFlags(&g_eng.copy_ev[i], cudaEventDisableTiming));
     CK(cudaMalloc(&g_eng.chunk_base, 17 * sizeof(int64_t)));
     CK(cudaHostAlloc((void **)&g_eng.hbase, 17 * sizeof(int64_t), cudaHostAllocMapped));
     CK(cudaMalloc(&g_eng.total, 256));
@@ -275,6 +276,26 @@ int alloc_pinned(size_t entries, PinnedBuf &out) {
     return DQMC_OK;
 }
 
+int grow_pinned(void **ptr, size_t &cap, size_t need, size_t elem) {
+    if (*ptr && need <= cap) return DQMC_OK;
+    if (*ptr) {
+        cudaFreeHost(*ptr);
+        *ptr = nullptr;
+        cap = 0;
+    }
+    const size_t want = std::max<size_t>(need, 1024);
+    cudaError_t e = cudaHostAlloc(ptr, want * elem, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        *ptr = nullptr;
+        char buf[160];
+        snprintf(buf, sizeof buf, "pinned host allocation of %llu bytes failed", (unsigned long long)(want * elem));
+        return set_err(DQMC_ERR_RESOURCE, buf);
+    }
+    cap = want;
+    return DQMC_OK;
+}
+
 int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_cap, uint32_t flags,
                      dqmc_result_t *out) {
     if (!out) return set_err(DQMC_ERR_INVALID, "null result pointer");
@@ -296,13 +317,13 @@ int primes_host_impl(const void *host_in, int kind, int n, int h, uint64_t mem_c
     if ((rc = engine_begin(s))) return rc;
     CK(cudaMemcpyAsync(g_eng.in_tmp, host_in, in_bytes, cudaMemcpyHostToDevice, s));
     const bool count_only = (flags & DQMC_FLAG_COUNT_ONLY) != 0;
-    // the chunked final stage overlaps the rank D2H with the last chunks'
-    // compute; it pays one host round trip per chunk (16), so it only runs
-    // when the hinted output is large enough for the overlap to win (>= 4M
-    // ranks = 32 MB; config 2's 0.4M ranks: 0.79 -> ~0.3 ms per call)
-    constexpr int64_t kPipelineMinRanks = (int64_t)1 << 22;
+    // the chunked final stage overlaps the packed rank D2H (4-byte tile
+    // offsets) and the host's widening to int64 with the last chunks' compute;
+    // it pays one host round trip per chunk (16), so it only runs when the
+    // hinted output is large enough for the overlap to win (>= 4M ranks =
+    // 32 MB; config 2's 0.4M ranks: 0.79 -> ~0.3 ms per call)
     const bool pipelined = !count_only && !(flags & (DQMC_FLAG_KEEP_BITMAP | DQMC_FLAG_TIMING)) && p.T > 0 &&
-                           g_eng.hint_n == n && g_eng.hint_count >= kPipelineMinRanks;
+                           g_eng.hint_n == n && g_eng.hint_count >= kPackedMinRanks;
     if (pipelined) {
         // merge/reduce passes, then the chunked final stage straight into pinned host memory
         g_eng.state_n = -1;  // the state is overwritten in the plan's own layout
@@ -394,7 +415,11 @@ int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *j
                 kind == DQMC_IN_U8 ? ((size_t)1 << n) : (size_t)std::max<int64_t>(1, (1ll << n) / 64) * 8;
             if ((rc = grow(g_eng.jin[slot], g_eng.jin_cap[slot], std::max<size_t>(in_bytes, 8), 1))) return rc;
             const size_t want = (size_t)((double)g_eng.hint_count * 1.05) + 4096;
-            if ((rc = grow(g_eng.jranks[slot], g_eng.jranks_cap[slot], want, 8))) return rc;
+            // large results stay packed in the slot (4-byte tile offsets in rank order)
+            const bool packed = g_eng.hint_count >= kPackedMinRanks;
+            const int64_t ntiles = pow3l(p.T);
+            if ((rc = grow(g_eng.jranks[slot], g_eng.jranks_cap[slot], packed ? (want + 1) / 2 : want, 8))) return rc;
+            if (packed && (rc = grow(g_eng.jpos[slot], g_eng.jpos_cap[slot], (size_t)ntiles, 8))) return rc;
             g_eng.scratch_want = std::max(g_eng.scratch_want, want);
             if ((rc = grow(g_eng.state, g_eng.state_cap, (size_t)p.sbytes, 1))) return rc;
             cudaStream_t s = g_eng.stream;
@@ -410,9 +435,12 @@ int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *j
             int64_t *cdev = g_eng.total + 8 + slot;  // device count of this slot (-(count+1): outputs too small)
             FinalOpts fo;
             fo.count_dev = cdev;
-            if ((rc = run_final(p, nullptr, g_eng.state, p.ib_E, -p.rank_sub, g_eng.jranks[slot],
-                                (int64_t)g_eng.jranks_cap[slot], false, fo, &unused, tm, s)))
+            if (packed) fo.packed32 = (uint32_t *)g_eng.jranks[slot];
+            if ((rc = run_final(p, nullptr, g_eng.state, p.ib_E, -p.rank_sub, packed ? nullptr : g_eng.jranks[slot],
+                                (int64_t)g_eng.jranks_cap[slot] * (packed ? 2 : 1), false, fo, &unused, tm, s)))
                 return rc;
+            if (packed)  // the next job's final stage rewrites the engine's tile positions
+                CK(cudaMemcpyAsync(g_eng.jpos[slot], g_eng.tile_pos, (size_t)ntiles * 8, cudaMemcpyDeviceToDevice, s));
             CK(cudaMemcpyAsync(g_eng.jcount_host + slot, cdev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
             CK(cudaEventRecord(g_eng.jev[slot], s));
             if ((rc = engine_done(s))) return rc;
@@ -423,6 +451,10 @@ int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *j
             j.kind = kind;
             j.n = n;
             j.flags = flags;
+            j.packed = packed;
+            j.ntiles = ntiles;
+            j.tile_cells = pow3l(p.g) * 243;
+            j.rank_add = -p.rank_sub;
             g_eng.jobs.push_back(j);
             *job_out = id;
             return DQMC_OK;
@@ -436,6 +468,38 @@ int submit_impl(const void *host_in, int kind, int n, uint32_t flags, int64_t *j
     j.res = res;
     g_eng.jobs.push_back(j);
     *job_out = j.id;
+    return DQMC_OK;
+}
+
+// A packed job's result: the tile positions first (they say where every
+// tile's offsets lie), then the offsets in 16 chunks of about equal size on
+// the copy stream; each chunk is widened to int64 ranks by the host threads
+// as soon as it has landed, while the copy engine moves the next one.
+static int collect_packed(const Job &j, int64_t c, int64_t *host) {
+    int rc;
+    if ((rc = grow_pinned((void **)&g_eng.stage32, g_eng.stage32_cap, (size_t)c, 4))) return rc;
+    if ((rc = grow_pinned((void **)&g_eng.stage_pos, g_eng.stage_pos_cap, (size_t)j.ntiles, 8))) return rc;
+    const uint32_t *dev32 = (const uint32_t *)g_eng.jranks[j.slot];
+    int64_t *pos = g_eng.stage_pos;
+    cudaStream_t s2 = g_eng.stream2;
+    CK(cudaMemcpyAsync(pos, g_eng.jpos[j.slot], (size_t)j.ntiles * 8, cudaMemcpyDeviceToHost, s2));
+    CK(cudaStreamSynchronize(s2));
+    const int K = (int)std::min<int64_t>(16, j.ntiles);
+    int64_t tb[17], at[17];  // chunk k: tiles [tb[k], tb[k+1]), entries [at[k], at[k+1])
+    for (int k = 0; k <= K; k++) {
+        tb[k] = k == 0 ? 0 : (k == K ? j.ntiles : std::lower_bound(pos, pos + j.ntiles, c / K * k) - pos);
+        at[k] = tb[k] < j.ntiles ? pos[tb[k]] : c;
+    }
+    for (int k = 0; k < K; k++) {
+        if (at[k + 1] > at[k])
+            CK(cudaMemcpyAsync(g_eng.stage32 + at[k], dev32 + at[k], (size_t)(at[k + 1] - at[k]) * 4,
+                               cudaMemcpyDeviceToHost, s2));
+        CK(cudaEventRecord(g_eng.copy_ev[k], s2));
+    }
+    for (int k = 0; k < K; k++) {
+        CK(cudaEventSynchronize(g_eng.copy_ev[k]));
+        host_widen(g_eng.stage32, host, pos + tb[k], 0, at[k + 1], tb[k], tb[k + 1], j.tile_cells, j.rank_add);
+    }
     return DQMC_OK;
 }
 
@@ -466,8 +530,15 @@ int collect_impl(int64_t job, dqmc_result_t *out) {
         PinnedBuf pb;
         int rc;
         if ((rc = alloc_pinned((size_t)c, pb))) return rc;
-        CK(cudaMemcpyAsync(pb.ptr, g_eng.jranks[j.slot], (size_t)c * 8, cudaMemcpyDeviceToHost, g_eng.stream2));
-        CK(cudaStreamSynchronize(g_eng.stream2));
+        if (j.packed) {
+            if ((rc = collect_packed(j, c, pb.ptr))) {
+                g_eng.free_pinned.push_back(pb);
+                return rc;
+            }
+        } else {
+            CK(cudaMemcpyAsync(pb.ptr, g_eng.jranks[j.slot], (size_t)c * 8, cudaMemcpyDeviceToHost, g_eng.stream2));
+            CK(cudaStreamSynchronize(g_eng.stream2));
+        }
         out->count = c;
         out->ranks = pb.ptr;
         out->_owner = new PinnedBuf(pb);
@@ -522,6 +593,13 @@ int dqmc_primes_tt(const uint64_t *tt_words, int n, int h, uint64_t mem_cap, uin
 
 int dqmc_primes_u8(const uint8_t *values, int n, int h, uint64_t mem_cap, uint32_t flags, dqmc_result_t *out) {
     return primes_host_impl(values, DQMC_IN_U8, n, h, mem_cap, flags, out);
+}
+
+int dqmc_host_threads(int n) { return host_widen_threads(n); }
+
+void dqmc_widen_host(const uint32_t *off32, int64_t *out, const int64_t *pos, int64_t add, int64_t end, int64_t t0,
+                     int64_t t1, int64_t tile_cells, int64_t rank_add) {
+    host_widen(off32, out, pos, add, end, t0, t1, tile_cells, rank_add);
 }
 
 void dqmc_free_result(dqmc_result_t *res) {
@@ -644,13 +722,18 @@ void dqmc_release(void) {
     for (auto &b : g_eng.free_pinned) cudaFreeHost(b.ptr);
     if (g_eng.stream) cudaStreamDestroy(g_eng.stream);
     if (g_eng.stream2) cudaStreamDestroy(g_eng.stream2);
-    for (int i = 0; i < 16; i++)
+    for (int i = 0; i < 16; i++) {
         if (g_eng.chunk_ev[i]) cudaEventDestroy(g_eng.chunk_ev[i]);
+        if (g_eng.copy_ev[i]) cudaEventDestroy(g_eng.copy_ev[i]);
+    }
+    if (g_eng.stage32) cudaFreeHost(g_eng.stage32);
+    if (g_eng.stage_pos) cudaFreeHost(g_eng.stage_pos);
     cudaFree(g_eng.chunk_base);
     if (g_eng.hbase) cudaFreeHost(g_eng.hbase);
     for (int i = 0; i < kJobSlots; i++) {
         cudaFree(g_eng.jin[i]);
         cudaFree(g_eng.jranks[i]);
+        cudaFree(g_eng.jpos[i]);
         if (g_eng.jev[i]) cudaEventDestroy(g_eng.jev[i]);
     }
     if (g_eng.jcount_host) cudaFreeHost(g_eng.jcount_host);

@@ -627,9 +627,13 @@ __global__ void k_publish_count(const int64_t *__restrict__ total, int64_t limit
     *dst = t <= limit ? t : -(t + 1);
 }
 
+// OutT = int64_t: final ranks (the tile's first rank added). OutT = uint32_t:
+// the packed form of the host API's large results, tile-relative offsets in
+// rank order; the host adds the tile's first rank (dqmc_hostpack.cpp).
+template <typename OutT>
 __global__ void __launch_bounds__(256) k_reorder(const uint32_t *__restrict__ scratch, const int64_t *__restrict__ base,
                                                  const int32_t *__restrict__ cnt, const int64_t *__restrict__ pos,
-                                                 const int64_t *__restrict__ rank0, int64_t *__restrict__ out,
+                                                 const int64_t *__restrict__ rank0, OutT *__restrict__ out,
                                                  int64_t cap, int64_t ntiles, int64_t scap,
                                                  const int64_t *__restrict__ dbase = nullptr) {
     const int lane = threadIdx.x & 31;
@@ -638,7 +642,8 @@ __global__ void __launch_bounds__(256) k_reorder(const uint32_t *__restrict__ sc
     const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
     for (int64_t t = w; t < ntiles; t += nw) {
         const int c = cnt[t];
-        const int64_t src = base[t], dst = pos[t] + add, r0 = rank0[t];
+        const int64_t src = base[t], dst = pos[t] + add;
+        const OutT r0 = sizeof(OutT) == 8 ? (OutT)rank0[t] : (OutT)0;
         // a tile whose range overflowed the scratch is skipped: the host sees
         // total > scratch capacity, grows the scratch and reruns the final stage
         if (c < 0 || src < 0 || src + c > scap) continue;
@@ -931,8 +936,13 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     }
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
-        k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos,
-                                       g_eng.tile_rank0, ranks, cap, ntiles, (int64_t)g_eng.scratch_cap);
+        if (o.packed32)
+            k_reorder<uint32_t><<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos,
+                                                     g_eng.tile_rank0, o.packed32, cap, ntiles,
+                                                     (int64_t)g_eng.scratch_cap);
+        else
+            k_reorder<int64_t><<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos,
+                                                    g_eng.tile_rank0, ranks, cap, ntiles, (int64_t)g_eng.scratch_cap);
         CK(cudaGetLastError());
         tm.mark("k_reorder", (uint64_t)ntiles * 16);
     }
@@ -988,12 +998,15 @@ int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, 
     return DQMC_OK;
 }
 
-// Host-API final stage, pipelined: the tiles are finished in K chunks on the
-// compute stream (E, scan, running base, reorder into the device rank
-// buffer); as soon as chunk c's event fires the host queues its D2H copy on
-// the copy stream, so the copy engine moves chunk c while the SMs finish
-// chunk c+1. Returns the total; *host_ok is false if the host buffer (sized
-// from the previous call) was too small.
+// Host-API final stage, pipelined and packed: the tiles are finished in K
+// chunks on the compute stream (E, scan, running base, reorder of the 4-byte
+// tile offsets into rank order). As soon as chunk c's event fires the host
+// queues the D2H of its tile positions and offsets on the copy stream, and as
+// soon as that copy has landed the host threads widen the chunk to int64
+// ranks (dqmc_hostpack.cpp) — the SMs finish chunk c+2 while the copy engine
+// moves chunk c+1 and the host widens chunk c. Half the PCIe bytes of int64
+// ranks. Returns the total; *host_ok is false if the host buffer (sized from
+// the previous call) was too small.
 int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int64_t host_cap, int64_t *count,
                         bool *host_ok, cudaStream_t s) {
     const int64_t ntiles = pow3l(p.T);
@@ -1002,9 +1015,13 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
     if ((rc = grow(g_eng.tile_base, g_eng.tile_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_pos, g_eng.tile_pos_cap, (size_t)ntiles, 8))) return rc;
     if ((rc = grow(g_eng.tile_cnt, g_eng.tile_cnt_cap, (size_t)ntiles, 4))) return rc;
-    if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)host_cap, 8))) return rc;
+    if ((rc = grow(g_eng.ranks, g_eng.ranks_cap, (size_t)(host_cap + 1) / 2, 8))) return rc;
+    if ((rc = grow_pinned((void **)&g_eng.stage32, g_eng.stage32_cap, (size_t)host_cap, 4))) return rc;
+    if ((rc = grow_pinned((void **)&g_eng.stage_pos, g_eng.stage_pos_cap, (size_t)ntiles, 8))) return rc;
+    uint32_t *ranks32 = (uint32_t *)g_eng.ranks;  // rank-ordered tile offsets on the device
     int64_t *hbase = g_eng.hbase;  // mapped pinned mirror of the chunk bases
     const int64_t slot = tile_slot(p), ovf0 = slot * ntiles;
+    const int64_t tile_cells = pow3l(p.g) * 243;
     for (int attempt = 0; attempt < 2; attempt++) {
         const size_t want = (size_t)ovf0 + std::max<size_t>(g_eng.scratch_want, (size_t)1 << 20);
         if ((rc = grow(g_eng.scratch, g_eng.scratch_cap, want, 4))) return rc;
@@ -1043,21 +1060,46 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
                                              hbase + c);
             CK(cudaGetLastError());
             const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 8);
-            k_reorder<<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
-                                           g_eng.tile_pos + t0, g_eng.tile_rank0 + t0, g_eng.ranks, host_cap, t1 - t0,
-                                           (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
+            k_reorder<uint32_t><<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
+                                                     g_eng.tile_pos + t0, g_eng.tile_rank0 + t0, ranks32, host_cap,
+                                                     t1 - t0, (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
             CK(cudaGetLastError());
             CK(cudaEventRecord(g_eng.chunk_ev[c], s));
         }
-        // copy-out as chunks complete (copy engine, overlapped with later chunks)
+        // copy-out and widening as chunks complete
         bool fits = true;
-        for (int c = 0; c < K; c++) {
-            CK(cudaEventSynchronize(g_eng.chunk_ev[c]));
-            const int64_t lo = hbase[c], hi = hbase[c + 1];
-            if (hi > host_cap) fits = false;
-            if (fits && hi > lo)
-                CK(cudaMemcpyAsync(host + lo, g_eng.ranks + lo, (size_t)(hi - lo) * 8, cudaMemcpyDeviceToHost,
-                                   g_eng.stream2));
+        int issued = 0, widened = 0;
+        auto ready = [](cudaEvent_t ev) {
+            if (cudaEventQuery(ev) == cudaSuccess) return true;
+            (void)cudaGetLastError();  // cudaErrorNotReady
+            return false;
+        };
+        while (widened < K) {
+            while (issued < K && ready(g_eng.chunk_ev[issued])) {
+                const int c = issued++;
+                const int64_t t0 = ntiles * c / K, t1 = ntiles * (c + 1) / K;
+                const int64_t lo = hbase[c], hi = hbase[c + 1];
+                if (hi > host_cap) fits = false;
+                if (fits) {
+                    CK(cudaMemcpyAsync(g_eng.stage_pos + t0, g_eng.tile_pos + t0, (size_t)(t1 - t0) * 8,
+                                       cudaMemcpyDeviceToHost, g_eng.stream2));
+                    if (hi > lo)
+                        CK(cudaMemcpyAsync(g_eng.stage32 + lo, ranks32 + lo, (size_t)(hi - lo) * 4,
+                                           cudaMemcpyDeviceToHost, g_eng.stream2));
+                }
+                CK(cudaEventRecord(g_eng.copy_ev[c], g_eng.stream2));
+            }
+            if (widened < issued && (issued == K || ready(g_eng.copy_ev[widened]))) {
+                const int c = widened++;
+                CK(cudaEventSynchronize(g_eng.copy_ev[c]));
+                if (fits) {
+                    const int64_t t0 = ntiles * c / K, t1 = ntiles * (c + 1) / K;
+                    host_widen(g_eng.stage32, host, g_eng.stage_pos + t0, hbase[c], hbase[c + 1], t0, t1, tile_cells,
+                               -p.rank_sub);
+                }
+                continue;
+            }
+            if (issued < K) CK(cudaEventSynchronize(g_eng.chunk_ev[issued]));
         }
         int64_t used = 0;
         CK(cudaMemcpyAsync(&used, g_eng.alloc, 8, cudaMemcpyDeviceToHost, s));

@@ -382,6 +382,10 @@ struct Job {
     const void *in = nullptr;
     int kind = 0, n = 0;
     uint32_t flags = 0;
+    // packed rank transfer (large results): the slot holds 4-byte tile offsets
+    // in rank order and the tiles' positions; collect widens them on the host
+    bool packed = false;
+    int64_t ntiles = 0, tile_cells = 0, rank_add = 0;
 };
 
 // Jobs in flight on the host API stream: with three, the next call's passes are
@@ -409,6 +413,11 @@ struct Engine {
     size_t cub_tmp_cap = 0;
     cudaStream_t stream2 = nullptr;   // copy-out stream of the pipelined host API
     cudaEvent_t chunk_ev[17] = {};
+    cudaEvent_t copy_ev[17] = {};     // packed rank transfer: chunk c's D2H has landed
+    uint32_t *stage32 = nullptr;      // pinned host staging of the packed offsets
+    size_t stage32_cap = 0;           // entries
+    int64_t *stage_pos = nullptr;     // pinned host copy of the tile positions
+    size_t stage_pos_cap = 0;         // entries
     int64_t *chunk_base = nullptr;    // device running bases of the chunked final stage
     int64_t *hbase = nullptr;         // mapped pinned host mirror of chunk_base
     int hint_n = -1;
@@ -439,6 +448,8 @@ struct Engine {
     size_t jin_cap[kJobSlots] = {};  // bytes
     int64_t *jranks[kJobSlots] = {};
     size_t jranks_cap[kJobSlots] = {};  // entries
+    int64_t *jpos[kJobSlots] = {};      // packed jobs: the slot's copy of the tile positions
+    size_t jpos_cap[kJobSlots] = {};    // entries
     int64_t *jcount_host = nullptr;  // pinned, one count per slot
     cudaEvent_t jev[kJobSlots] = {};
     // ordering between entry points: every call that enqueues work on the
@@ -559,6 +570,8 @@ struct FinalOpts {
     const uint64_t *kill_tab = nullptr;     // per state: kMaxKill parent addresses (FinalArgs.kill_tab)
     const int64_t *rank_add_tab = nullptr;  // per state: rank of its first cell
     bool skip_c0 = false;                   // the C0 axes are already reduced
+    uint32_t *packed32 = nullptr;           // multi-tile: write rank-ordered 4-byte tile offsets here (cap entries)
+                                            // instead of int64 ranks (the host widens them, dqmc_hostpack.cpp)
     int64_t *slot_start = nullptr;          // per state: offset / count of its ranks in the output
     int64_t *slot_count = nullptr;
 };
@@ -570,5 +583,14 @@ int run_final_retry(const Plan &p, const uint32_t *tt32, const uint32_t *state, 
                     cudaStream_t s);
 int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int64_t host_cap, int64_t *count,
                         bool *host_ok, cudaStream_t s);
+
+// results of at least this many ranks (32 MB of int64) take the chunked,
+// packed host paths; smaller ones one plain int64 copy
+constexpr int64_t kPackedMinRanks = (int64_t)1 << 22;
+int grow_pinned(void **ptr, size_t &cap, size_t need, size_t elem);  // pinned host staging (kept until release)
+// dqmc_hostpack.cpp: widen packed tile offsets to int64 ranks on the host thread pool
+void host_widen(const uint32_t *off32, int64_t *out, const int64_t *pos, int64_t add, int64_t end, int64_t t0,
+                int64_t t1, int64_t tile_cells, int64_t rank_add);
+int host_widen_threads(int n);
 
 }  // namespace dqmc

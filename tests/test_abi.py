@@ -42,7 +42,7 @@ def test_abi_version_and_sizes(pkg):
     from paper_2302_10083_b200 import _lib
 
     L = _lib.load()
-    assert L.dqmc_abi_version() == 3
+    assert L.dqmc_abi_version() == 4
     for h in range(1, 10):
         assert L.dqmc_block_bits(h) == pkg.block_bits_for(h)
     for n in range(1, 28):
@@ -131,3 +131,37 @@ def test_sparse_cap_validated_before_the_device(pkg):
     assert pkg.ENGINES == ("dense", "sparse")
     with pytest.raises(ValueError, match="oracle"):
         pkg.run_engine("oracle", tt)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_widen_host_matches_numpy(pkg, threads):
+    """The host half of the packed rank transfer (csrc/dqmc_hostpack.cpp):
+    rank = tile's first rank + 4-byte offset, every tile boundary, empty
+    tiles, unaligned output and chunk-relative positions, any pool size."""
+    from paper_2302_10083_b200 import _lib
+
+    L = _lib.load()
+    prev = L.dqmc_host_threads(threads)
+    try:
+        rng = np.random.default_rng(7 + threads)
+        tile_cells, rank_add = 3**12, -162
+        for ntiles, mean in ((1, 5), (50, 3), (3000, 40), (2000, 700)):
+            cnt = rng.poisson(mean, ntiles).astype(np.int64)
+            cnt[rng.random(ntiles) < 0.2] = 0  # zero tiles
+            t0, add = 17, 12345  # a chunk in the middle of a call
+            pos = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+            total = int(cnt.sum())
+            end = add + total
+            off = np.zeros(end + 5, dtype=np.uint32)
+            off[add:end] = rng.integers(0, tile_cells, total, dtype=np.uint32)
+            for shift in (0, 1, 3):  # output alignment relative to 64 bytes
+                buf = np.full(end + 16, -7, dtype=np.int64)
+                out = buf[shift:]
+                L.dqmc_widen_host(off.ctypes.data, out.ctypes.data, pos.ctypes.data, add, end, t0, t0 + ntiles,
+                                  tile_cells, rank_add)
+                tile_of = np.repeat(np.arange(ntiles, dtype=np.int64), cnt)
+                want = (t0 + tile_of) * tile_cells + rank_add + off[add:end].astype(np.int64)
+                assert np.array_equal(out[add:end], want)
+                assert np.all(out[:add] == -7) and np.all(out[end:] == -7)  # nothing outside the chunk
+    finally:
+        L.dqmc_host_threads(prev)

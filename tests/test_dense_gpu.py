@@ -378,6 +378,23 @@ class TestJobStream:
             assert len(got[i]) == g["primes"] and rsha(got[i])[:16] == g["ranks_sha256_prefix"]
         assert len(got[2]) == c5 and rsha(got[2]) == h5
 
+    @pytest.mark.parametrize("threads", [0, 1, 5])
+    def test_stream_packed_transfer(self, pkg, oracle_mod, gen_mod, threads):
+        """Results of 4M+ ranks leave the device as 4-byte tile offsets and are
+        widened to int64 by the host pool (n = 20 here: ~6M ranks): different
+        tables back to back, any pool size, equal to the oracle."""
+        from paper_2302_10083_b200 import _lib
+
+        prev = _lib.load().dqmc_host_threads(threads)
+        try:
+            tabs = [gen_mod.gen3(20, 0.8, 0.05, s) for s in (21, 22, 23, 24)]
+            got = list(pkg.stream_prime_ranks(tabs))
+            for t, g in zip(tabs, got):
+                assert g.dtype == np.int64 and len(g) >= 1 << 22
+                assert np.array_equal(g, oracle_mod.dense_prime_ranks(gen_mod.values_to_words(t), 20))
+        finally:
+            _lib.load().dqmc_host_threads(prev)
+
     def test_truth_tables_and_repeat(self, pkg, gen_mod):
         t = pkg.TruthTable(17, gen_mod.random_words(17, 0.6, 9))
         want = pkg.dense_prime_ranks(t)
