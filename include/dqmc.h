@@ -46,7 +46,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DQMC_ABI_VERSION 4
+#define DQMC_ABI_VERSION 5
 
 /* status codes */
 #define DQMC_OK 0
@@ -256,6 +256,21 @@ void dqmc_release(void);
 uint64_t dqmc_engine_generation(void);
 int dqmc_engine_enter(void *stream);
 int dqmc_engine_exit(void *stream);
+
+/* The n = 24 plan (two strided groups of six axes) finishes a state one of two
+ * ways, chosen on the device from the number of nonzero 256-bit blocks its
+ * merge+reduce pass wrote: the read+write REDUCE pass of the lower group
+ * (run_pass(REDUCE, dim), dense.py:296-315, one sweep per axis there), or, for
+ * sparse states, the "gather finish": that pass is not run and the final stage
+ * reads the lower group's parents of each surviving block straight from the
+ * state (same result: REDUCE from unreduced parents, dense.py:46-53).
+ * dqmc_gather_threshold sets the choice: gather when at most `permille` of
+ * every 1000 blocks are nonzero (0 = never, 1000 = always, < 0 = query only);
+ * returns the previous setting. dqmc_last_gather reports the block count of
+ * the last finished call of that plan and whether it took the gather finish
+ * (synchronises the device; DQMC_ERR_INVALID if no such call ran). */
+int dqmc_gather_threshold(int permille);
+int dqmc_last_gather(int64_t *nonzero_blocks, int64_t *total_blocks, int *gathered);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -762,4 +762,25 @@ int dqmc_engine_exit(void *stream) {
     return engine_done((cudaStream_t)stream);
 }
 
+int dqmc_gather_threshold(int permille) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int prev = g_eng.gather_permille;
+    if (permille >= 0) g_eng.gather_permille = std::min(permille, 1000);
+    return prev;
+}
+
+int dqmc_last_gather(int64_t *nonzero_blocks, int64_t *total_blocks, int *gathered) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_eng.gather_n < 0 || !g_eng.nzflags) return set_err(DQMC_ERR_INVALID, "no call of the two-group plan has run");
+    const Plan p = make_plan(g_eng.gather_n);
+    const size_t npiece = (size_t)(p.pitch / kRowBlocks), nr = (size_t)pow3l(p.r[0]);
+    unsigned long long c = 0;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&c, g_eng.nzflags + nz_count_offset(npiece, nr), 8, cudaMemcpyDeviceToHost));
+    if (nonzero_blocks) *nonzero_blocks = (int64_t)c;
+    if (total_blocks) *total_blocks = p.nblocks;
+    if (gathered) *gathered = c <= g_eng.gather_limit_last;
+    return DQMC_OK;
+}
+
 }  // extern "C"

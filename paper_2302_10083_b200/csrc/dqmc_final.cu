@@ -53,6 +53,40 @@ __device__ void tile_reduce_c0(uint32_t *sm, int g) {
 }
 
 
+// Gather finish: group-0 kills of block b of tile (u, l) read from the state.
+// gb = the tile's piece 0 at row l; piece x = b / 4 is x * nr rows further;
+// goff[j] = (2 - d_j) 3^j rows in words (0: digit j of l is already 2, no
+// parent). Every lane reads a different 32-B sector: one 256-bit load per
+// parent (the cost is the L1 tag stage, one lookup per lane and instruction).
+struct Blk256 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ Blk256 ld256_nc(const uint32_t *p) {
+    Blk256 r;
+    // no L1 allocation: a parent sector is used once per tile (12.3 vs 12.7 ms)
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                   "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void g0_kill(const uint32_t *__restrict__ gb, int nr32, const int *goff, int b,
+                                        uint32_t (&v)[8]) {
+    const uint32_t *p = gb + (b >> 2) * nr32 + (b & 3) * 8;
+    uint32_t k[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < kGroupMax; j++) {
+        const int o = goff[j];
+        if (o) {
+            const Blk256 a = ld256_nc(p + o);
+#pragma unroll
+            for (int i = 0; i < 8; i++) k[i] |= a.w[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) v[i] &= ~k[i];
+}
+
 // In-block reduce, popcount and ordered compaction of one tile
 // (dense.py:376-397 extract_ranks: rank = block*243 + bit; memory order is
 // rank order, so the output needs no sort). Warp w owns the contiguous block
@@ -88,7 +122,8 @@ struct FinishSmem {
 
 template <int NT>
 __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, int64_t blk0, const FinalArgs &fa,
-                                            FinishSmem<NT> &fs) {
+                                            FinishSmem<NT> &fs, const uint32_t *gb = nullptr, int nr32 = 0,
+                                            const int *goff = nullptr) {
     constexpr int kMaxIter = finish_iters<NT>();
     constexpr int kPk = (kMaxIter + 1) / 2;
     int64_t *s_warp_off = fs.warp_off;
@@ -98,6 +133,7 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
     constexpr int nwarps = NT / 32;  // compile-time: the range split needs no runtime division
     const int b0 = nb * warp / nwarps, b1 = nb * (warp + 1) / nwarps;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
+    const uint32_t ibm = fa.ib_mask | (gb ? fa.ib_gather : 0u);  // gather finish: pass D's in-block axes too
 
     // (1) lane = block: popcount (+ in-block axes, kills, bitmap on the slow path)
     uint32_t pk[kPk];
@@ -108,7 +144,7 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
     const int64_t slot_blk0 = slot * fa.tiles_per_slot * nb;  // first block of the slot
     const int64_t rank_add = fa.rank_add_tab ? fa.rank_add_tab[slot] - slot_blk0 * 243 : fa.rank_add;
     const uint64_t *kills = fa.kill_tab ? fa.kill_tab + slot * kMaxKill : nullptr;
-    if (!fa.ib_mask && !kills && !fa.bitmap_out) {  // count only: word order does not matter
+    if (!ibm && !kills && !fa.bitmap_out && !gb) {  // count only: word order does not matter
 #pragma unroll
         for (int j = 0; j < kMaxIter; j++) {
             const int b = b0 + 32 * j + lane;
@@ -130,9 +166,9 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
                 uint4 *p = reinterpret_cast<uint4 *>(sm + b * 8);
                 const uint4 ya = p[h], yb = p[h ^ 1];
                 uint4 x0 = h ? yb : ya, x1 = h ? ya : yb;
-                if (fa.ib_mask) {
+                if (ibm) {
                     uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                    inblock_reduce(v, fa.ib_mask);
+                    inblock_reduce(v, ibm);
                     x0 = make_uint4(v[0], v[1], v[2], v[3]);
                     x1 = make_uint4(v[4], v[5], v[6], v[7]);
                 }
@@ -156,7 +192,13 @@ __device__ __forceinline__ void tile_finish(uint32_t *sm, int nb, int64_t tile, 
                     x0 = make_uint4(x0.x & ~k0.x, x0.y & ~k0.y, x0.z & ~k0.z, x0.w & ~k0.w);
                     x1 = make_uint4(x1.x & ~k1.x, x1.y & ~k1.y, x1.z & ~k1.z, x1.w & ~k1.w);
                 }
-                if (fa.ib_mask || kills) {
+                if (gb && (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w)) {
+                    uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    g0_kill(gb, nr32, goff, b, v);
+                    x0 = make_uint4(v[0], v[1], v[2], v[3]);
+                    x1 = make_uint4(v[4], v[5], v[6], v[7]);
+                }
+                if (ibm || kills || gb) {
                     p[h] = h ? x1 : x0;
                     p[h ^ 1] = h ? x0 : x1;
                 }
@@ -394,7 +436,9 @@ constexpr int kSparseMax = 600;
 
 template <int NT, int G, bool SHARD>
 __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t tile, int64_t blk0,
-                                                   const FinalArgs &fa, FinishSmem<NT> &fs) {
+                                                   const FinalArgs &fa, FinishSmem<NT> &fs,
+                                                   const uint32_t *gb = nullptr, int nr32 = 0,
+                                                   const int *goff = nullptr) {
     constexpr int NB = pow3i(G);
     constexpr int NWARP = NT / 32;
     constexpr int kMaxIter = ((NB + NWARP - 1) / NWARP + 31) / 32;
@@ -409,6 +453,7 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = (lane >> 2) & 1;  // half-swap: conflict-free LDS.128 at 32-B lane stride
     const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t ibm = fa.ib_mask | (gb ? fa.ib_gather : 0u);  // gather finish: pass D's in-block axes too
     // SHARD (the sharded extract): this tile's super-block (slot), its parents
     // and rank offset; the fused plans compile none of it
     const int64_t slot = SHARD && (fa.kill_tab || fa.rank_add_tab) ? tile / fa.tiles_per_slot : 0;
@@ -470,10 +515,13 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
         if (e < ntot) {
             int w, idx;
             entry(e, w, idx);
-            if (SHARD)
-                finish_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa, kills, kofs, v);
-            else
-                prime_block<G>(sm, NB * w / NWARP + s_lst[w][idx], fa.ib_mask, v);
+            const int blk = NB * w / NWARP + s_lst[w][idx];
+            if (SHARD) {
+                finish_block<G>(sm, blk, fa, kills, kofs, v);
+            } else {
+                prime_block<G>(sm, blk, ibm, v);
+                if (gb && (v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7])) g0_kill(gb, nr32, goff, blk, v);
+            }
 #pragma unroll
             for (int k = 0; k < 8; k++) c += __popc(v[k]);
             s_lcnt[w][idx] = (uint8_t)c;
@@ -522,10 +570,12 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
             cnt = s_lcnt[w][idx];
             b = NB * w / NWARP + s_lst[w][idx];
             if (bt != warp && cnt) {
-                if (SHARD)
+                if (SHARD) {
                     finish_block<G>(sm, b, fa, kills, kofs, v);
-                else
-                    prime_block<G>(sm, b, fa.ib_mask, v);
+                } else {
+                    prime_block<G>(sm, b, ibm, v);
+                    if (gb) g0_kill(gb, nr32, goff, b, v);
+                }
             }
         }
         int incl = cnt;
@@ -712,7 +762,9 @@ __device__ __forceinline__ void tile_reduce_c0_t(uint32_t *sm) {
 // pass E: one CTA per C0 tile (3^G blocks); the tile arrives in shared
 // memory with one TMA bulk copy (or three 4-D tensor boxes, piece-major).
 
-template <int G>
+// GATH (the n = 24 plan): the kernel also holds the gather finish and takes it
+// when pass C left a sparse state (gather_chosen); pass D then returned at once.
+template <int G, bool GATH = false>
 __global__ void __launch_bounds__(kFinalThreads, 3)
     k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa, const __grid_constant__ CUtensorMap ma,
                const __grid_constant__ CUtensorMap mb) {
@@ -741,6 +793,18 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
             if (fa.tile_rank0) fa.tile_rank0[tile] = blk0 * 243 + fa.rank_add;
         }
         return;
+    }
+    __shared__ int s_goff[kGroupMax];
+    const uint32_t *gb = nullptr;
+    if (GATH && gather_chosen(fa.g0_cnt, fa.g0_limit)) {  // gather finish: this tile's group-0 parents, rows (2 - d_j) 3^j up in every D item
+        const uint32_t t32 = (uint32_t)tile, nr = (uint32_t)fa.pm_nr;
+        const uint32_t u = t32 / nr, l = t32 - u * nr;
+        gb = fa.g0 + ((int64_t)u * fa.pm_np * nr + l) * 32;
+        if (threadIdx.x >= 64 && threadIdx.x < 64 + kGroupMax) {
+            const int j = threadIdx.x - 64;
+            const int p3 = (int)pow3l(j), d = (int)(l / p3) % 3;
+            s_goff[j] = d != 2 ? (2 - d) * p3 * 32 : 0;
+        }
     }
     if (threadIdx.x == 0 && fa.pm_nr) {
         // piece-major group 0: the tile is pm_np pieces 3^r pieces apart; boxes
@@ -783,12 +847,12 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     if (!fa.bitmap_out) {
         if (fa.kill_tab || fa.skip_c0 || fa.rank_add_tab) {
             if (tile_finish_sparse<kFinalThreads, G, true>(sm, tile, blk0, fa, fs)) return;
-        } else if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs)) {
+        } else if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff)) {
             return;
         }
     }
     if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
-    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa, fs);
+    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff);
 }
 
 // n <= 12: the whole problem is one tile; one CTA does A and E.
@@ -836,8 +900,14 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
     case G:                                                                             \
         k_c0_final<G><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);  \
         break;
-        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
+        case 7:
+            if (fa.g0)
+                k_c0_final<7, true><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);
+            else
+                k_c0_final<7><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);
+            break;
         default: return set_err(DQMC_ERR_INVALID, "bad tile exponent");
     }
     CK(cudaGetLastError());
@@ -848,6 +918,27 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
 // every tile a fixed range (2.2 GB at 1024 entries; config 4 averages ~485
 // primes per nonzero tile), so most tiles reserve nothing with an atomic.
 int64_t tile_slot(const Plan &p) { return p.nz ? 1024 : 0; }
+}  // namespace
+
+// Gather finish (Plan::nz): at most this many nonzero blocks after pass C
+unsigned long long gather_limit(const Plan &p) {
+    if (!p.nz) return 0ull;
+    if (g_eng.gather_permille >= 1000) return ~0ull;
+    return (unsigned long long)p.nblocks * (unsigned long long)g_eng.gather_permille / 1000ull;
+}
+
+namespace {
+// the final stage's gather arguments: the state, pass C's block count, the limit
+void set_gather(const Plan &p, const uint32_t *state, FinalArgs &fa) {
+    if (!p.nz || !fa.nz_e || g_eng.gather_permille == 0) return;  // never: pass D got limit 0 and ran
+    const size_t npiece = (size_t)(p.pitch / kRowBlocks), nr = (size_t)pow3l(p.r[0]);
+    fa.g0 = state;
+    fa.g0_cnt = reinterpret_cast<const unsigned long long *>(g_eng.nzflags + nz_count_offset(npiece, nr));
+    fa.g0_limit = gather_limit(p);
+    fa.ib_gather = p.ib_D[0];
+}
+}  // namespace
+namespace {
 
 // E's zero-skip flags: written by pass C of the same fused plan on the engine state
 const uint32_t *nz_e_flags(const Plan &p, const uint32_t *state) {
@@ -903,6 +994,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     fa.pitch = p.pitch;
     fa.prefetch = 3 * g_eng.num_sms;  // one generation of resident CTAs (3 per SM): 9.23 -> 9.0 ms at n=24
     fa.nz_e = nz_e_flags(p, state);
+    set_gather(p, state, fa);
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
     if (tt32) {
         k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
@@ -1042,6 +1134,7 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
         fa.prefetch = 3 * g_eng.num_sms;
         fa.pitch = p.pitch;
         fa.nz_e = nz_e_flags(p, state);
+        set_gather(p, state, fa);
         CUtensorMap ma, mb;
         if ((rc = make_final_maps(p, state, &ma, &mb, fa))) return rc;
         CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
@@ -1117,6 +1210,7 @@ int final_set_attrs() {
     const int tile_smem = (int)pow3l(kC0Max) * 32;
     // + one 128-B piece (the padded pitch of a piece-major tile, make_plan) + 128 B of alignment
     CK(cudaFuncSetAttribute(k_c0_final<kC0Max>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem + 256));
+    CK(cudaFuncSetAttribute(k_c0_final<kC0Max, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem + 256));
     CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
     return DQMC_OK;
 }

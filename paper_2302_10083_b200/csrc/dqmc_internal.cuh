@@ -105,7 +105,20 @@ struct FinalArgs {
     const uint32_t *nz_e = nullptr;  // zero-tile flags (Plan::nz): bit u of row l = tile (u, l) may be nonzero
     int slot = 0;                    // per-tile scratch slot (entries); 0: every tile reserves with an atomic
     int64_t ovf0 = 0;                // first entry of the overflow pool (after the slots)
+    // gather finish (Plan::nz, sparse states): pass D is not run; the group-0
+    // parents of every block that survives the C0 reduce are read from the
+    // state itself (piece-major: the same D item, (2 - d_j) 3^j rows up)
+    // It is chosen on the device: pass C counts the nonzero blocks it wrote
+    // (g0_cnt); the gather runs when they are at most g0_limit, else pass D ran.
+    const uint32_t *g0 = nullptr;
+    const unsigned long long *g0_cnt = nullptr;
+    unsigned long long g0_limit = 0;
+    uint32_t ib_gather = 0;  // in-block axes pass D would have reduced
 };
+// device-side choice between pass D and the gather finish (both kernels evaluate it)
+__device__ __forceinline__ bool gather_chosen(const unsigned long long *cnt, unsigned long long limit) {
+    return cnt != nullptr && __ldg(cnt) <= limit;
+}
 
 // ---------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, SASS UBLKCP) with an mbarrier
@@ -343,11 +356,16 @@ struct Plan {
 // are kNzWords words. REDUCE only clears bits, so a zero flag is exact for D
 // and E.
 constexpr int kNzWords = 24;
+constexpr int kGatherPermille = 350;  // default dqmc_gather_threshold
 // Flag layout in g_eng.nzflags (npiece = pieces per C0 tile, nr = 3^6 group-0
 // rows): nz_b [npiece][3 boxes of 243 rows][kNzWords] (pass D's items (x, u)
 // per box), nz_e [nr][kNzWords] (pass E's tiles (u, l)), then a zero page of
 // one 243-row box (128-B aligned) that pass D loads its all-zero boxes from.
 inline size_t nz_e_offset(size_t npiece) { return npiece * 3 * kNzWords; }
+// ... then pass C's count of nonzero blocks (one unsigned long long)
+inline size_t nz_count_offset(size_t npiece, size_t nr) {
+    return (((npiece * 3 + nr) * kNzWords + 31) & ~(size_t)31) + (nr / 3) * 32;
+}
 inline size_t nz_zero_page(size_t npiece, size_t nr) { return ((npiece * 3 + nr) * kNzWords + 31) & ~(size_t)31; }
 
 Plan make_plan(int n, bool padded = true);
@@ -460,6 +478,11 @@ struct Engine {
     // bumped whenever a workspace buffer is (re)allocated or released:
     // captured CUDA graphs hold raw pointers and must not replay across it
     uint64_t generation = 1;
+    // gather finish (Plan::nz): taken when pass C wrote at most this many
+    // nonzero blocks per 1000 (dqmc_gather_threshold; 0 = never, 1000 = always)
+    int gather_permille = kGatherPermille;
+    int gather_n = -1;                         // n of the last call whose pass C counted blocks
+    unsigned long long gather_limit_last = 0;  // its limit
 };
 
 extern Engine g_eng;
@@ -563,6 +586,7 @@ int nz_account(const Plan &p, Timer &tm, cudaStream_t s);
 
 // final stage E (dqmc_final.cu)
 int final_set_attrs();
+unsigned long long gather_limit(const Plan &p);
 struct FinalOpts {
     uint32_t *bitmap_out = nullptr;         // write the final bitmap (reference layout)
     int64_t *count_dev = nullptr;           // DQMC_FLAG_ASYNC: publish the count here, no host sync

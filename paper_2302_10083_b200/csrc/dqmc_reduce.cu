@@ -19,7 +19,8 @@ template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     k_strided_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
                    int64_t ncol, int64_t nitems, uint32_t ib_mask, int pm, int sparse,
-                   const uint32_t *__restrict__ nz_b) {
+                   const uint32_t *__restrict__ nz_b, const unsigned long long *__restrict__ g0_cnt,
+                   unsigned long long g0_limit) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2;
     constexpr int NR = SM::NR;
@@ -27,6 +28,8 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS, 1)
     constexpr int CC = pipe_cols<R1, R2>(), PITCH = SM::PITCH;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t full[2], computed[2];
+    // sparse state: the final stage gathers this group's parents itself (FinalArgs::g0)
+    if (gather_chosen(g0_cnt, g0_limit)) return;
     // 4-D map coordinates of an item: reference layout {col words, row, outer, 0};
     // piece-major group 0 (pm, CC = 1) {0, row, col, outer} (make_group_map4)
     auto crd = [&](int64_t it, int &c0, int &c2, int &c3) {
@@ -201,7 +204,7 @@ template <int R1, int R2>
 __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
     k_merge_reduce_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap,
                         int64_t ncol, int64_t nitems, uint32_t ib_mask, int sparse, uint32_t *__restrict__ nz_b,
-                        uint32_t *__restrict__ nz_e, int nz_nr) {
+                        uint32_t *__restrict__ nz_e, int nz_nr, unsigned long long *__restrict__ nz_cnt) {
     using SM = PipeSmem<R1, R2>;
     constexpr int N1 = SM::N1, N2 = SM::N2, B1 = 1 << R1, B2 = 1 << R2;
     constexpr int NR = SM::NR;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
         return;
     }
     if (warp == CW + 1) {  // ------------------------------ store warp
+        unsigned nblk = 0;  // nonzero blocks this CTA wrote (chooses pass D or the gather finish)
         for (int64_t i = 0; i < L; i++) {
             const int b = (int)(i & 1);
             const int64_t it = blockIdx.x + i * gridDim.x;
@@ -260,7 +264,11 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
                 const int nw = (NR * kRowBlocks + 31) / 32;
 #pragma unroll
                 for (int q = 0; q < 4; q++)
-                    if (4 * lane + q < nw) w |= or4_compact(s_blk[b][4 * lane + q]) << (8 * q);
+                    if (4 * lane + q < nw) {
+                        const uint32_t m = s_blk[b][4 * lane + q];
+                        w |= or4_compact(m) << (8 * q);
+                        nblk += __popc(m);
+                    }
                 // D item (x, u), E tile (u, l); dense inputs: most bits are
                 // already set, so read first (in flight during the wait below)
                 fd = &nz_b[((col / nz_nr) * 3 + (col % nz_nr) / (nz_nr / 3)) * kNzWords + lane];
@@ -274,6 +282,11 @@ __global__ void __launch_bounds__(PipeSmem<R1, R2>::THREADS + 32, 1)
             }
             if ((od & w) != w) atomicOr(fd, w);
             if ((oe & w) != w) atomicOr(fe, w);
+        }
+        if (nz_cnt) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nblk += __shfl_xor_sync(0xffffffffu, nblk, o);
+            if (lane == 0) atomicAdd(nz_cnt, (unsigned long long)nblk);
         }
         if (lane == 0) bulk_wait0();
         return;
@@ -420,7 +433,7 @@ int make_gather_map(CUtensorMap *map, uint32_t *state, int64_t Q, int r1, int r2
 
 template <int R1, int R2, int MODE>
 int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, bool pm, cudaStream_t s,
-                uint32_t *nz) {
+                uint32_t *nz, unsigned long long g0_limit) {
     using SM = PipeSmem<R1, R2>;
     constexpr int CC = pipe_cols<R1, R2>();  // 128-B columns per tile
     CUtensorMap map, gmap;
@@ -440,7 +453,10 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
     if (MODE == MERGE_REDUCE)
         k_merge_reduce_pipe<R1, R2><<<grid, SM::THREADS + 32, SM::SMEM, s>>>(
             map, gmap, ncolg, nitems, ib, kSparseSkip, nz, nz ? nz + nz_e_offset(Q / kRowBlocks / pow3l(R1 + R2)) : nullptr,
-            P3<R1 + R2>::v);
+            P3<R1 + R2>::v,
+            nz ? reinterpret_cast<unsigned long long *>(
+                     nz + nz_count_offset((size_t)(Q / kRowBlocks / pow3l(R1 + R2)), (size_t)P3<R1 + R2>::v))
+               : nullptr);
     else
     {
         CUtensorMap zmap;  // zero-skip mode: the zero page, box {32, BOXR} (a fully-specified map otherwise unused)
@@ -457,7 +473,11 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
             if (r != CUDA_SUCCESS) return set_err(DQMC_ERR_CUDA, "cuTensorMapEncodeTiled (zero page) failed: " + std::to_string((int)r));
         }
         k_strided_pipe<R1, R2><<<grid, SM::THREADS, SM::SMEM, s>>>(map, zmap, ncolg, nitems, ib, pm ? 1 : 0,
-                                                                   kSparseSkip, nz);
+                                                                   kSparseSkip, nz,
+                                                                   nz ? reinterpret_cast<const unsigned long long *>(
+                                                                            nz + nz_count_offset((size_t)ncolg, (size_t)SM::NR))
+                                                                      : nullptr,
+                                                                   g0_limit);
     }
     CK(cudaGetLastError());
     return DQMC_OK;
@@ -465,14 +485,14 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
 
 template <int MODE>
 int launch_pipe_mode(int r, uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32_t ib, cudaStream_t s,
-                     bool pm = false, uint32_t *nz = nullptr) {
+                     bool pm = false, uint32_t *nz = nullptr, unsigned long long g0_limit = 0) {
     switch (r) {
-        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
-        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
-        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
-        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
-        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr);
-        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s, nz);
+        case 1: return launch_pipe<1, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr, 0);
+        case 2: return launch_pipe<2, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr, 0);
+        case 3: return launch_pipe<3, 0, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr, 0);
+        case 4: return launch_pipe<2, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr, 0);
+        case 5: return launch_pipe<3, 2, MODE>(state, Q, ncol, nouter, ib, pm, s, nullptr, 0);
+        default: return launch_pipe<3, 3, MODE>(state, Q, ncol, nouter, ib, pm, s, nz, g0_limit);
     }
 }
 
@@ -512,9 +532,13 @@ int nz_account(const Plan &p, Timer &tm, cudaStream_t s) {
     CK(cudaMemsetAsync(cnt, 0, 16, s));
     k_nz_count<<<1, 1024, 0, s>>>(g_eng.nzflags, nd, ne, cnt);
     CK(cudaGetLastError());
-    unsigned long long h[2] = {0, 0};
+    unsigned long long h[2] = {0, 0}, nblk = 0;
     CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&nblk, g_eng.nzflags + nz_count_offset((size_t)npiece, (size_t)nr), 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    // gather finish: pass D returned at once; the final stage read the group-0
+    // parents of its surviving blocks from L2 (no algorithmic HBM bytes)
+    if (nblk <= g_eng.gather_limit_last) h[0] = 0;
     const uint64_t box_d = (uint64_t)(nr / 3) * 128, tile_e = (uint64_t)p.pitch * 32;
     int last_d = -1, e = -1;
     for (size_t i = 0; i < tm.names.size(); i++) {
@@ -549,16 +573,20 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         const size_t npiece = (size_t)(p.pitch / kRowBlocks), nr = (size_t)pow3l(p.r[0]);
         nz_words = (npiece * 3 + nr) * kNzWords;  // nz_b, nz_e: zeroed per call
         const size_t zp = nz_zero_page(npiece, nr), zwords = (nr / 3) * 32;
-        if ((rc = grow(g_eng.nzflags, g_eng.nzflags_cap, zp + zwords, 4))) return rc;
+        if ((rc = grow(g_eng.nzflags, g_eng.nzflags_cap, zp + zwords + 2, 4))) return rc;
         nz = g_eng.nzflags;
-        CK(cudaMemsetAsync(nz + zp, 0, zwords * 4, s));
+        CK(cudaMemsetAsync(nz + zp, 0, (zwords + 2) * 4, s));  // the zero page and pass C's block count
     }
     {
         const int k = p.m - 1;
         const int64_t Q = pow3l(p.a[k] - p.g) * p.pitch;
         const int64_t ncol = (Q + kRowBlocks - 1) / kRowBlocks;
         if (fused) {
-            if (nz) CK(cudaMemsetAsync(nz, 0, nz_words * 4, s));
+            if (nz) {
+                CK(cudaMemsetAsync(nz, 0, nz_words * 4, s));
+                g_eng.gather_n = p.n;
+                g_eng.gather_limit_last = gather_limit(p);
+            }
             if ((rc = launch_pipe_mode<MERGE_REDUCE>(p.r[k], state, Q, ncol, 1, p.ib_C, s, false, nz))) return rc;
             tm.mark("k_strided<MERGE_REDUCE>", (uint64_t)(S * std::pow(2.0 / 3.0, p.r[k]) + S));
         } else {
@@ -572,7 +600,8 @@ int run_reduce(const Plan &p, uint32_t *state, bool fused, Timer &tm, cudaStream
         int above = 0;
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
         if ((rc = launch_pipe_mode<REDUCE_ONLY>(p.r[k], state, Q, ncol, pow3l(above) * nbatch, p.ib_D[k], s,
-                                                k == 0 && p.pm, k == 0 ? nz : nullptr)))
+                                                k == 0 && p.pm, k == 0 ? nz : nullptr,
+                                                k == 0 && nz ? gather_limit(p) : 0)))
             return rc;
         tm.mark("k_strided<REDUCE>", 2 * S);
     }

@@ -42,7 +42,7 @@ def test_abi_version_and_sizes(pkg):
     from paper_2302_10083_b200 import _lib
 
     L = _lib.load()
-    assert L.dqmc_abi_version() == 4
+    assert L.dqmc_abi_version() == 5
     for h in range(1, 10):
         assert L.dqmc_block_bits(h) == pkg.block_bits_for(h)
     for n in range(1, 28):

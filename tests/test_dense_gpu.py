@@ -252,6 +252,47 @@ class TestFullSize:
         del out, r1
         torch.cuda.empty_cache()
 
+    @pytest.mark.parametrize("p_on,p_dc,seed", [(0.75, 0.05, 3), (0.9, 0.0, 5), (0.99, 0.0, 4)])
+    def test_n24_gather_finish_equals_pass_d(self, pkg, golden, p_on, p_dc, seed):
+        """The two ways the n=24 plan finishes a state (include/dqmc.h,
+        dqmc_gather_threshold): the lower group's REDUCE as its own read+write
+        pass D, or gathered in the final stage from the unreduced state. Both
+        forced on the same table, sparse to config-5 density: identical rank
+        lists (config 4: the reference's count and hash), and the device-side
+        choice reports what it did."""
+        import ctypes
+
+        from paper_2302_10083_b200 import _lib, device
+
+        L = _lib.load()
+        v = device.gen3_device(24, p_on, p_dc, seed)
+        prev = L.dqmc_gather_threshold(-1)
+
+        def info():
+            nzb, tot, g = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int(0)
+            _lib.check(L.dqmc_last_gather(ctypes.byref(nzb), ctypes.byref(tot), ctypes.byref(g)))
+            return nzb.value, tot.value, g.value
+
+        try:
+            L.dqmc_gather_threshold(0)  # never: pass D
+            r0, c0 = device.dense_prime_ranks_device(v, 24)
+            nzb, tot, g = info()
+            assert tot == 3**19 and 0 < nzb <= tot and g == 0
+            L.dqmc_gather_threshold(1000)  # always: gather finish
+            r1, c1 = device.dense_prime_ranks_device(v, 24)
+            assert info() == (nzb, tot, 1)
+            assert c1 == c0 and bool(r1.eq(r0).all())
+            if (p_on, seed) == (0.75, 3):
+                g4 = golden["configs"]["4"]
+                assert c1 == g4["primes"] and rsha(r1.cpu().numpy())[:16] == g4["ranks_sha256_prefix"]
+            del r0
+            L.dqmc_gather_threshold(prev)  # the default choice follows the block density
+            r2, c2 = device.dense_prime_ranks_device(v, 24)
+            assert info()[2] == (1 if nzb * 1000 <= tot * prev else 0)
+            assert c2 == c1 and bool(r2.eq(r1).all())
+        finally:
+            L.dqmc_gather_threshold(prev)
+
 
 @pytest.mark.slow
 class TestLargestSingleGpu:

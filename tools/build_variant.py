@@ -19,9 +19,13 @@ os.makedirs(os.path.dirname(out), exist_ok=True)
 
 
 def one(src):
-    o = os.path.join(obj, src.replace(".cu", ".o"))
-    r = subprocess.run([ge._nvcc(), *ge.NVCC_FLAGS, *defs, "-c", "-o", o, os.path.join(ge.CSRC, src)], cwd=ge.CSRC,
-                       capture_output=True, text=True)
+    o = os.path.join(obj, os.path.splitext(src)[0] + ".o")
+    if src.endswith(".cpp"):  # host-only unit
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-pthread", *defs, "-c", "-o", o,
+               os.path.join(ge.CSRC, src)]
+    else:
+        cmd = [ge._nvcc(), *ge.NVCC_FLAGS, *defs, "-c", "-o", o, os.path.join(ge.CSRC, src)]
+    r = subprocess.run(cmd, cwd=ge.CSRC, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         raise SystemExit(f"nvcc failed on {src}")
