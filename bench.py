@@ -600,6 +600,19 @@ def run_engine_bench(args):
         cpu["one_thread_n24"] = one_thread_n24()
 
     traffic = load_ncu_traffic(dom)
+    # how the plan finished the state (include/dqmc.h, dqmc_last_gather): sparse states skip
+    # the read+write pass D and gather the lower group's parents in the final stage
+    import ctypes
+
+    nzb, totb, gath = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int(0)
+    L = _lib.load()
+    if L.dqmc_last_gather(ctypes.byref(nzb), ctypes.byref(totb), ctypes.byref(gath)) == 0:
+        finish = {"kind": "gather" if gath.value else "pass_d", "nonzero_blocks": nzb.value,
+                  "blocks": totb.value, "threshold_permille": int(L.dqmc_gather_threshold(-1))}
+    else:
+        finish = None
+    # the whole step against the floor of reading the table and writing + reading the state once
+    floor_ms = ((1 << n) / 8 + 2 * pkg.state_bytes(n, 5)) / (peak * 1e9) * 1e3
     line = {
         "metric": METRIC,
         "value": value,
@@ -662,6 +675,10 @@ def run_engine_bench(args):
             for k in tot
         },
         "all_passes_gbs": all_bytes / (all_ms / 1e3) / 1e9,
+        "all_passes_bytes": all_bytes,
+        "finish": finish,
+        "step_floor": {"ms": floor_ms, "what": "truth table read + state written once and read once, at the measured "
+                       "copy peak", "step_over_floor": t_step * 1e3 / floor_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "configs": configs,

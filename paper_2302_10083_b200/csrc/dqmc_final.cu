@@ -438,7 +438,10 @@ template <int NT, int G, bool SHARD>
 __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t tile, int64_t blk0,
                                                    const FinalArgs &fa, FinishSmem<NT> &fs,
                                                    const uint32_t *gb = nullptr, int nr32 = 0,
-                                                   const int *goff = nullptr) {
+                                                   const int *goff = nullptr, bool reduced = false) {
+    // reduced (gather finish, dense tiles): the C0 axes are already reduced
+    // in shared memory (tile_reduce_c0_t); list and finish whatever is left
+    const int smax = reduced ? pow3i(G) : kSparseMax;
     constexpr int NB = pow3i(G);
     constexpr int NWARP = NT / 32;
     constexpr int kMaxIter = ((NB + NWARP - 1) / NWARP + 31) / 32;
@@ -477,7 +480,7 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
                 const uint4 x0 = p[h], x1 = p[h ^ 1];
                 nz = (x0.x | x0.y | x0.z | x0.w | x1.x | x1.y | x1.z | x1.w) != 0u;
             }
-            if (j == 0 && kMaxIter > 1 && __syncthreads_count(nz) > kSparseMax * 32 * NWARP / NB) return false;
+            if (j == 0 && kMaxIter > 1 && __syncthreads_count(nz) > smax * 32 * NWARP / NB) return false;
             const uint32_t m = __ballot_sync(0xffffffffu, nz);
             if (nz) s_lst[warp][n + __popc(m & lt)] = (typename FinishSmem<NT>::Idx)(32 * j + lane);
             n += __popc(m);
@@ -488,7 +491,7 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
     int ntot = 0;
 #pragma unroll
     for (int w = 1; w <= NWARP; w++) ntot += s_off[w];
-    if (ntot > kSparseMax) return false;
+    if (ntot > smax) return false;
     if (threadIdx.x == 0) {  // list offsets of the warps' ranges (s_off is still being read)
         int acc = 0;
         for (int w = 0; w < NWARP; w++) s_pre[w] = acc, acc += s_off[w + 1];
@@ -519,7 +522,14 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
             if (SHARD) {
                 finish_block<G>(sm, blk, fa, kills, kofs, v);
             } else {
-                prime_block<G>(sm, blk, ibm, v);
+                if (reduced) {
+                    const uint4 *p = reinterpret_cast<const uint4 *>(sm + blk * 8);
+                    const uint4 a0 = p[0], a1 = p[1];
+                    v[0] = a0.x, v[1] = a0.y, v[2] = a0.z, v[3] = a0.w, v[4] = a1.x, v[5] = a1.y, v[6] = a1.z, v[7] = a1.w;
+                    if (ibm) inblock_reduce(v, ibm);
+                } else {
+                    prime_block<G>(sm, blk, ibm, v);
+                }
                 if (gb && (v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7])) g0_kill(gb, nr32, goff, blk, v);
             }
 #pragma unroll
@@ -573,7 +583,15 @@ __device__ __forceinline__ bool tile_finish_sparse(const uint32_t *sm, int64_t t
                 if (SHARD) {
                     finish_block<G>(sm, b, fa, kills, kofs, v);
                 } else {
-                    prime_block<G>(sm, b, ibm, v);
+                    if (reduced) {
+                        const uint4 *p = reinterpret_cast<const uint4 *>(sm + b * 8);
+                        const uint4 a0 = p[0], a1 = p[1];
+                        v[0] = a0.x, v[1] = a0.y, v[2] = a0.z, v[3] = a0.w, v[4] = a1.x, v[5] = a1.y, v[6] = a1.z,
+                        v[7] = a1.w;
+                        if (ibm) inblock_reduce(v, ibm);
+                    } else {
+                        prime_block<G>(sm, b, ibm, v);
+                    }
                     if (gb) g0_kill(gb, nr32, goff, b, v);
                 }
             }
@@ -796,7 +814,8 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     }
     __shared__ int s_goff[kGroupMax];
     const uint32_t *gb = nullptr;
-    if (GATH && gather_chosen(fa.g0_cnt, fa.g0_limit)) {  // gather finish: this tile's group-0 parents, rows (2 - d_j) 3^j up in every D item
+    // gather finish: this tile's group-0 parents, rows (2 - d_j) 3^j up in every D item
+    if (GATH && gather_chosen(fa.g0_cnt, fa.g0_limit)) {
         const uint32_t t32 = (uint32_t)tile, nr = (uint32_t)fa.pm_nr;
         const uint32_t u = t32 / nr, l = t32 - u * nr;
         gb = fa.g0 + ((int64_t)u * fa.pm_np * nr + l) * 32;
@@ -847,8 +866,15 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     if (!fa.bitmap_out) {
         if (fa.kill_tab || fa.skip_c0 || fa.rank_add_tab) {
             if (tile_finish_sparse<kFinalThreads, G, true>(sm, tile, blk0, fa, fs)) return;
-        } else if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff)) {
-            return;
+        } else {
+            // gather finish: a dense tile goes through the register-cube rounds and
+            // then the same batched finish over the blocks the rounds left
+            for (bool reduced = false;; reduced = true) {
+                if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff, reduced))
+                    return;
+                if (!GATH || !gb) break;
+                tile_reduce_c0_t<G, 0>(sm);
+            }
         }
     }
     if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
