@@ -822,7 +822,9 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
         if (threadIdx.x >= 64 && threadIdx.x < 64 + kGroupMax) {
             const int j = threadIdx.x - 64;
             const int p3 = (int)pow3l(j), d = (int)(l / p3) % 3;
-            s_goff[j] = d != 2 ? (2 - d) * p3 * 32 : 0;
+            // a parent tile that pass C flagged all zero kills nothing: no loads for it
+            const bool none = d == 2 || tile_zero((int64_t)u * nr + l + (2 - d) * p3);
+            s_goff[j] = none ? 0 : (2 - d) * p3 * 32;
         }
     }
     if (threadIdx.x == 0 && fa.pm_nr) {
