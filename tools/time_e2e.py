@@ -1,13 +1,16 @@
 """Host-to-host timing of the n=24 config-4 call: the synchronous drop-in call and the job
 stream (three in flight), for several sizes of the host widening pool (packed rank transfer).
-usage: python tools/time_e2e.py [n] [threads ...]"""
+usage: [DQMC_LIB=variant.so] python tools/time_e2e.py [n] [threads ...]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import hashlib
 import numpy as np
 import torch
 import paper_2302_10083_b200 as pkg
-from paper_2302_10083_b200 import device, _lib
+from paper_2302_10083_b200 import _lib
+if os.environ.get("DQMC_LIB"):  # a tools/build_variant.py build
+    _lib.LIB_PATH = os.path.abspath(os.environ["DQMC_LIB"])
+from paper_2302_10083_b200 import device
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 threads = [int(x) for x in sys.argv[2:]] or [0]
