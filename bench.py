@@ -475,7 +475,8 @@ def run_engine_bench(args):
     if world > 1:
         from paper_2302_10083_b200 import sharded
 
-        return sharded.bench_main(args, WORKLOAD, METRIC, UNIT)
+        return sharded.bench_main(args, {**WORKLOAD, "name": WORKLOAD_NAME + "; sharded on the top log2(N) variables"},
+                                  METRIC, UNIT, clock_sampler=ClockSampler)
     torch.cuda.set_device(local)
 
     dev = torch.device(f"cuda:{local}")
@@ -499,11 +500,14 @@ def run_engine_bench(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        launches0 = int(_lib.load().dqmc_launch_count())
         ev0.record(stream)
         for i in range(args.steps):
             device.enqueue_prime_ranks(values, n, out, cnt_dev[i : i + 1])
         ev1.record(stream)
         torch.cuda.synchronize()
+        # the library counts its own kernel launches (dqmc_launch_count)
+        timed_launches = int(_lib.load().dqmc_launch_count()) - launches0
     assert cnt_dev.eq(cnt).all().item(), cnt_dev.tolist()
     t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
     value = 3**n / t_step
@@ -679,7 +683,9 @@ def run_engine_bench(args):
         "finish": finish,
         "step_floor": {"ms": floor_ms, "what": "truth table read + state written once and read once, at the measured "
                        "copy peak", "step_over_floor": t_step * 1e3 / floor_ms},
-        "gpu_launches": launches,
+        "gpu_launches": timed_launches,
+        "gpu_launches_what": "libdqmc's own kernels launched inside the timed region of `value` (counted by the "
+                             "library, dqmc_launch_count); CUB's scan kernels are library launches and not counted",
         "clocks": clk.summary(),
         "configs": configs,
         "next_rows": next_rows,

@@ -270,6 +270,10 @@ int dqmc_engine_exit(void *stream);
  * the last finished call of that plan and whether it took the gather finish
  * (synchronises the device; DQMC_ERR_INVALID if no such call ran). */
 int dqmc_gather_threshold(int permille);
+/* Kernels this library has launched so far in this process (its own CUDA
+ * kernels of the dense, sharded, sparse and input paths; the per-dimension
+ * state API and library calls such as CUB scans are not counted). */
+uint64_t dqmc_launch_count(void);
 int dqmc_last_gather(int64_t *nonzero_blocks, int64_t *total_blocks, int *gathered);
 
 #if defined(__GNUC__)

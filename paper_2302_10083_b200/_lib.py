@@ -75,6 +75,7 @@ EXPORTS = (
     "dqmc_engine_exit",
     "dqmc_gather_threshold",
     "dqmc_last_gather",
+    "dqmc_launch_count",
     "dqmc_sparse_primes_tt",
     "dqmc_state_create",
     "dqmc_state_free",
@@ -179,6 +180,7 @@ def load() -> ctypes.CDLL:
             "dqmc_engine_enter": (i32, [vp]),
             "dqmc_engine_exit": (i32, [vp]),
             "dqmc_gather_threshold": (i32, [i32]),
+            "dqmc_launch_count": (u64, []),
             "dqmc_last_gather": (i32, [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                        ctypes.POINTER(ctypes.c_int)]),
             "dqmc_sparse_primes_tt": (i32, [vp, i32, u64, ctypes.POINTER(DqmcResult)]),

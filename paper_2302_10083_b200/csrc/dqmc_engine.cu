@@ -11,6 +11,7 @@ thread_local std::string g_err;
 const bool g_debug = getenv("DQMC_DEBUG") != nullptr;  // sync + report after every pass
 std::mutex g_mu;
 Engine g_eng;
+std::atomic<uint64_t> g_launches{0};
 
 // padded: each C0 tile of 3^g blocks is stored at a pitch rounded up to a
 // multiple of 4 blocks (128 B; 2187 -> 2188 blocks at g = 7) so that every
@@ -761,6 +762,8 @@ int dqmc_engine_exit(void *stream) {
     if ((rc = ensure_device())) return rc;
     return engine_done((cudaStream_t)stream);
 }
+
+uint64_t dqmc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int dqmc_gather_threshold(int permille) {
     std::lock_guard<std::mutex> lk(g_mu);

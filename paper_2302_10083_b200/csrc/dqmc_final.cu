@@ -938,7 +938,7 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
             break;
         default: return set_err(DQMC_ERR_INVALID, "bad tile exponent");
     }
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     return DQMC_OK;
 }
 
@@ -1026,7 +1026,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     CK(cudaMemsetAsync(g_eng.alloc, 0, 8, s));
     if (tt32) {
         k_small<<<1, kTileThreads, tile_smem, s>>>(tt32, p.g, fa);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         tm.mark("k_small", (uint64_t)(1ull << p.H) * 4 + (bitmap_out ? S : 0));
     } else {
         CUtensorMap ma, mb;
@@ -1036,7 +1036,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
     }
     if (ntiles <= 4096) {
         k_scan_tiles<<<1, 1024, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
     } else {
         // device-wide exclusive scan (CUB) of the int32 counts into int64 positions
         size_t tmp = 0;
@@ -1046,13 +1046,13 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
         CK(cub::DeviceScan::ExclusiveScan(g_eng.cub_tmp, tmp, g_eng.tile_cnt, g_eng.tile_pos, cub::Sum(), (int64_t)0,
                                           (int64_t)ntiles, s));
         k_scan_total<<<1, 32, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, ntiles, g_eng.total);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
     }
     tm.mark("k_scan_tiles", (uint64_t)ntiles * 12);
     if (o.slot_start && o.slot_count) {
         k_slot_spans<<<(unsigned)((nbatch + 255) / 256), 256, 0, s>>>(g_eng.tile_cnt, g_eng.tile_pos, tps, nbatch,
                                                                        o.slot_start, o.slot_count);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
     }
     if (!count_only && !direct) {
         const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)g_eng.num_sms * 16);
@@ -1063,7 +1063,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
         else
             k_reorder<int64_t><<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base, g_eng.tile_cnt, g_eng.tile_pos,
                                                     g_eng.tile_rank0, ranks, cap, ntiles, (int64_t)g_eng.scratch_cap);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         tm.mark("k_reorder", (uint64_t)ntiles * 16);
     }
     if (count_dev) {  // DQMC_FLAG_ASYNC: no host synchronisation
@@ -1071,7 +1071,7 @@ int run_final(const Plan &p, const uint32_t *tt32, const uint32_t *state, uint32
         const int64_t limit =
             count_only ? INT64_MAX : (direct ? cap : std::min<int64_t>(cap, (int64_t)g_eng.scratch_cap - ovf0));
         k_publish_count<<<1, 1, 0, s>>>(g_eng.total, limit, count_dev);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         return DQMC_OK;
     }
     int64_t total = 0;
@@ -1179,12 +1179,12 @@ int run_final_pipelined(const Plan &p, const uint32_t *state, int64_t *host, int
                                               (int64_t)0, (int64_t)(t1 - t0), s));
             k_chunk_advance<<<1, 32, 0, s>>>(g_eng.tile_cnt + t1 - 1, g_eng.tile_pos + t1 - 1, g_eng.chunk_base + c,
                                              hbase + c);
-            CK(cudaGetLastError());
+            CK_LAUNCH();
             const int grid = (int)std::min<int64_t>((t1 - t0 + 7) / 8, (int64_t)g_eng.num_sms * 8);
             k_reorder<uint32_t><<<grid, 256, 0, s>>>(g_eng.scratch, g_eng.tile_base + t0, g_eng.tile_cnt + t0,
                                                      g_eng.tile_pos + t0, g_eng.tile_rank0 + t0, ranks32, host_cap,
                                                      t1 - t0, (int64_t)g_eng.scratch_cap, g_eng.chunk_base + c);
-            CK(cudaGetLastError());
+            CK_LAUNCH();
             CK(cudaEventRecord(g_eng.chunk_ev[c], s));
         }
         // copy-out and widening as chunks complete

@@ -109,14 +109,14 @@ int input_words(const void *in, int kind, int n, const uint32_t **tt32, cudaStre
     if (n < 5) {
         if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, 256, 1))) return rc;
         k_pad_small<<<1, 32, 0, s>>>(in, kind, n, g_eng.tt_tmp);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         *tt32 = g_eng.tt_tmp;
     } else if (kind == DQMC_IN_U8) {
         const int64_t nw = 1ll << (n - 5);
         if ((rc = grow(g_eng.tt_tmp, g_eng.tt_tmp_cap, (size_t)nw * 4, 1))) return rc;
         const int grid = (int)std::min<int64_t>((nw * 32 + 255) / 256, 148ll * 32);
         k_u8_to_words<<<grid, 256, 0, s>>>((const uint8_t *)in, g_eng.tt_tmp, nw);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         *tt32 = g_eng.tt_tmp;
     } else {
         *tt32 = (const uint32_t *)in;  // LE uint64 words viewed as uint32 words
@@ -142,7 +142,7 @@ int dqmc_gen3_range_device(uint8_t *values_dev, int64_t x0, int64_t count, doubl
     const uint64_t t_any = (uint64_t)((p_on + p_dc) * 9007199254740992.0);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148ll * 64));
     if (count) k_gen3<<<grid, 256, 0, s>>>(values_dev, x0, count, seed, t_on, t_any);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     CK(cudaStreamSynchronize(s));
     return DQMC_OK;
 }
@@ -160,7 +160,7 @@ int dqmc_gen_sbox_device(uint8_t *values_dev, uint64_t seed, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(values_dev, 1, (size_t)1 << 20, s));
     k_sbox<<<1, 1024, 0, s>>>(values_dev, seed);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     CK(cudaStreamSynchronize(s));
     return DQMC_OK;
 }
@@ -211,7 +211,7 @@ int dqmc_order_by_weight(const int64_t *ranks_host, int64_t count, int n, int64_
     CK(cudaMemcpyAsync(r_in, ranks_host, (size_t)count * 8, cudaMemcpyHostToDevice, s));
     const int grid = (int)std::min<int64_t>((count + 255) / 256, 148ll * 32);
     k_weight_keys<<<grid, 256, 0, s>>>(r_in, count, n, k_in);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, k_in, k_out, r_in, r_out, (int)count, 0, 8, s));
     CK(cudaMalloc(&tmp, tmpb));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmpb, k_in, k_out, r_in, r_out, (int)count, 0, 8, s));

@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <cmath>
 #include <deque>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -383,6 +384,16 @@ inline int set_err(int code, const std::string &msg) {
     do {                                                                                                 \
         cudaError_t e_ = (call);                                                                         \
         if (e_ != cudaSuccess) return set_err(DQMC_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// every kernel launch of the dense, sharded, sparse and input paths is
+// checked through this macro and counted (dqmc_launch_count: the bench line's
+// gpu_launches)
+extern std::atomic<uint64_t> g_launches;
+#define CK_LAUNCH()                                  \
+    do {                                             \
+        g_launches.fetch_add(1, std::memory_order_relaxed); \
+        CK(cudaGetLastError());                      \
     } while (0)
 
 struct PinnedBuf {

@@ -152,7 +152,7 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
     const int64_t ntA = 1ll << p.T;
     const int gridA = (int)std::min<int64_t>(ntA, (int64_t)g_eng.num_sms * 8);
     k_c0_merge<<<gridA, kTileThreads, tile_smem, s>>>(tt32, state, p.g, p.T, p.pitch, p.pm ? p.r[0] : 0);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     tm.mark("k_c0_merge", (uint64_t)ntA * ((1ull << p.g) * 4 + (uint64_t)pow3l(p.g) * 32));
     auto frac = [&](int k) { return (double)S * std::pow(2.0 / 3.0, k); };
     const int last = full ? p.m : p.m - 1;
@@ -163,7 +163,7 @@ int run_merge(const Plan &p, const uint32_t *tt32, uint32_t *state, bool full, T
         for (int j = k + 1; j < p.m; j++) above += p.r[j];
         const int64_t nitems = ncol << above;
         launch_strided_r(p.r[k], state, Q, ncol, nitems, k == 0 && p.pm, s);
-        CK(cudaGetLastError());
+        CK_LAUNCH();
         tm.mark("k_strided<MERGE_ONLY>", (uint64_t)frac(above));
     }
     return DQMC_OK;

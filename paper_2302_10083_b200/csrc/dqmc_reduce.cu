@@ -479,7 +479,7 @@ int launch_pipe(uint32_t *state, int64_t Q, int64_t ncol, int64_t nouter, uint32
                                                                       : nullptr,
                                                                    g0_limit);
     }
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     return DQMC_OK;
 }
 
@@ -531,7 +531,7 @@ int nz_account(const Plan &p, Timer &tm, cudaStream_t s) {
     unsigned long long *cnt = reinterpret_cast<unsigned long long *>(g_eng.total) + 4;
     CK(cudaMemsetAsync(cnt, 0, 16, s));
     k_nz_count<<<1, 1024, 0, s>>>(g_eng.nzflags, nd, ne, cnt);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     unsigned long long h[2] = {0, 0}, nblk = 0;
     CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&nblk, g_eng.nzflags + nz_count_offset((size_t)npiece, (size_t)nr), 8, cudaMemcpyDeviceToHost, s));

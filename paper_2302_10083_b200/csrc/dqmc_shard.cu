@@ -186,7 +186,7 @@ int dqmc_bitop_batch_device(const uint64_t *jobs_dev, int64_t njobs, uint64_t nb
     const int64_t want = ((int64_t)g_eng.num_sms * 16 + njobs - 1) / njobs;
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (n16 + 255) / 256));
     k_bitop_batch<<<dim3(gx, (unsigned)njobs), 256, 0, s>>>(jobs_dev, n16, op);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     return DQMC_OK;
 }
 
@@ -200,7 +200,7 @@ int dqmc_bitop_device(uint32_t *dst, const uint32_t *a, const uint32_t *b, uint6
     const int64_t n16 = (int64_t)(nbytes / 16);
     const int grid = (int)std::min<int64_t>((n16 + 255) / 256, 148ll * 16);
     if (n16) k_bitop<<<grid, 256, 0, s>>>((uint4 *)dst, (const uint4 *)a, (const uint4 *)b, n16, op);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     return DQMC_OK;
 }
 

@@ -234,7 +234,7 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
     CK(cudaMemcpyAsync(tt.p, tt_host, (size_t)nwords * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(cnt, 0, 8, s));
     k_sp_popcount<<<grid_of(nwords), 256, 0, s>>>((const uint64_t *)tt.p, nwords, cnt);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     const int64_t npts = read_count(cnt, s, &rc);
     if (rc) return rc;
     int64_t size = table_size(npts);
@@ -242,7 +242,7 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
     if ((rc = tabA.ensure((size_t)size * 8))) return rc;
     CK(cudaMemsetAsync(tabA.p, 0, (size_t)size * 8, s));
     k_sp_seed<<<grid_of(1ll << n), 256, 0, s>>>((const uint64_t *)tt.p, n, (uint64_t *)tabA.p, (uint64_t)(size - 1));
-    CK(cudaGetLastError());
+    CK_LAUNCH();
     DevBuf *cur = &tabA, *nxt = &tabB;
     int64_t ncap = std::max<int64_t>(npts, 1024), rcap = std::max<int64_t>(npts, 1024);
     int64_t total = 0;
@@ -256,7 +256,7 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
             CK(cudaMemsetAsync(cnt, 0, 8, s));
             k_sp_generate<<<grid_of(size), 256, 0, s>>>((const uint64_t *)cur->p, mask, size, n, (uint64_t *)cand.p,
                                                         ncap, cnt);
-            CK(cudaGetLastError());
+            CK_LAUNCH();
             ncand = read_count(cnt, s, &rc);
             if (rc) return rc;
             if (ncand <= ncap) break;
@@ -270,16 +270,16 @@ int sparse_impl(const uint64_t *tt_host, int n, uint64_t mem_cap, dqmc_result_t 
             CK(cudaMemsetAsync(nxt->p, 0, (size_t)nsize * 8, s));
             k_sp_insert<<<grid_of(ncand), 256, 0, s>>>((const uint64_t *)cand.p, ncand, (uint64_t *)nxt->p,
                                                        (uint64_t)(nsize - 1));
-            CK(cudaGetLastError());
+            CK_LAUNCH();
             k_sp_mark<<<grid_of(ncand), 256, 0, s>>>((const uint64_t *)cand.p, ncand, n, (uint64_t *)cur->p, mask);
-            CK(cudaGetLastError());
+            CK_LAUNCH();
         }
         // live cubes of this level are prime
         for (int attempt = 0; attempt < 2; attempt++) {
             CK(cudaMemsetAsync(cnt, 0, 8, s));
             k_sp_emit<<<grid_of(size), 256, 0, s>>>((const uint64_t *)cur->p, size, n, (int64_t *)ranks.p + total,
                                                     rcap - total, cnt);
-            CK(cudaGetLastError());
+            CK_LAUNCH();
             const int64_t got = read_count(cnt, s, &rc);
             if (rc) return rc;
             if (total + got <= rcap) {

@@ -525,7 +525,7 @@ def dry_run(n: int, k: int) -> dict:
 # bench.py under torchrun (N > 1)
 
 
-def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
+def bench_main(args, workload, metric, unit, clock_sampler=None):  # pragma: no cover - needs N GPUs
     """The workload sharded on the top log2(N) variables, one rank per GPU;
     CUDA-event time of the whole schedule, max over ranks. The same n at every
     N (total work fixed): strong scaling."""
@@ -578,12 +578,25 @@ def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = int(_lib.load().dqmc_launch_count())
+    clk = None
+    if clock_sampler is not None and rank == 0:  # SM clocks and throttle reasons during the timed region
+        try:
+            clk = clock_sampler(local % ndev)
+            clk.__enter__()
+        except Exception:
+            clk = None
     e0.record()
     parts = None
     for _ in range(args.steps):
         parts = step(vals)
     e1.record()
     torch.cuda.synchronize()
+    clocks = None
+    if clk is not None:
+        clk.__exit__(None, None, None)
+        clocks = clk.summary()
+    launches = int(_lib.load().dqmc_launch_count()) - launches0  # this rank's kernels in the timed region
     cnt = primes_of(parts)
     # e2e: this rank's slice from pinned host memory, its primes back to the host
     dist.barrier()
@@ -604,7 +617,7 @@ def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
     dev = "cuda" if backend == "nccl" else "cpu"
     t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps, e2.elapsed_time(e3) / 1e3 / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    c = torch.tensor([cnt, d2h], device=dev, dtype=torch.int64)
+    c = torch.tensor([cnt, d2h, launches], device=dev, dtype=torch.int64)
     dist.all_reduce(c)
     comm.close(ops)
     if rank == 0:
@@ -620,7 +633,8 @@ def bench_main(args, workload, metric, unit):  # pragma: no cover - needs N GPUs
                        "max_peak_device_bytes": b["max_peak_device_bytes"]},
             "e2e": {"value": 3**n / te2e, "unit": unit, "ms_per_step": te2e * 1e3,
                     "h2d_bytes_per_step": int(1 << n), "d2h_bytes_per_step": int(c[1].item())},
-            "gpu_launches": None,
+            "gpu_launches": int(c[2].item()),
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
