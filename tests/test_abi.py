@@ -54,6 +54,36 @@ def test_abi_version_and_sizes(pkg):
     assert pkg.state_bytes(3, 1) == 72 and pkg.state_bytes(20, 5) == 3**15 * 32
 
 
+def test_gather_threshold_and_launch_count(pkg):
+    """The tuning knob of the n=24 plan's finish (include/dqmc.h) is plain host
+    state: set/query round trip, clamped to 0..1000, no device needed; nothing
+    has run, so there is no gather report and no launch has been counted."""
+    import ctypes
+
+    from paper_2302_10083_b200 import _lib
+
+    L = _lib.load()
+    prev = L.dqmc_gather_threshold(-1)
+    try:
+        assert 0 <= prev <= 1000
+        assert L.dqmc_gather_threshold(0) == prev
+        assert L.dqmc_gather_threshold(5000) == 0
+        assert L.dqmc_gather_threshold(-1) == 1000
+    finally:
+        L.dqmc_gather_threshold(prev)
+    assert L.dqmc_gather_threshold(-1) == prev
+    if not pkg_has_device():
+        a, b, g = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int(0)
+        assert L.dqmc_last_gather(ctypes.byref(a), ctypes.byref(b), ctypes.byref(g)) == _lib.DQMC_ERR_INVALID
+        assert L.dqmc_launch_count() == 0
+
+
+def pkg_has_device() -> bool:
+    import torch
+
+    return torch.cuda.is_available()
+
+
 def test_plan_covers_every_axis(pkg):
     from paper_2302_10083_b200 import _lib
 

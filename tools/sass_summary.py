@@ -9,7 +9,7 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(REPO, "paper_2302_10083_b200", "libdqmc.so")
-HOT = ("k_strided_pipe<3, 3>", "k_merge_reduce_pipe<3, 3>", "k_c0_final<7>", "k_sp_generate")
+HOT = ("k_strided_pipe<3, 3>", "k_merge_reduce_pipe<3, 3>", "k_c0_final<7, false>", "k_c0_final<7, true>", "k_sp_generate")
 KEYS = ["LOP3", "SHF", "LDS", "STS", "LDG", "STG", "UTMALDG", "UTMASTG", "UBLKCP", "LDGSTS", "SYNCS", "POPC",
         "SHFL", "BAR", "IMAD", "IADD3", "ATOMG", "REDG"]
 
