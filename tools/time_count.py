@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Per-pass times of count-only n=24 calls (timing experiments whose results may be wrong).
-Usage: python tools/time_count.py LIB.so [p_on]"""
+Usage: python tools/time_count.py LIB.so [p_on] [gather_permille]"""
 import os
 import sys
 
@@ -11,6 +11,8 @@ _lib.LIB_PATH = os.path.abspath(sys.argv[1])
 from paper_2302_10083_b200 import device  # noqa: E402
 
 p_on = float(sys.argv[2]) if len(sys.argv) > 2 else 0.75
+if len(sys.argv) > 3:
+    _lib.load().dqmc_gather_threshold(int(sys.argv[3]))
 v = device.gen3_device(24, p_on, 0.05 if p_on == 0.75 else 0.0, 3)
 acc = {}
 for i in range(5):
