@@ -792,8 +792,13 @@ __device__ __forceinline__ void tile_reduce_c0_t(uint32_t *sm) {
 
 // GATH (the n = 24 plan): the kernel also holds the gather finish and takes it
 // when pass C left a sparse state (gather_chosen); pass D then returned at once.
-template <int G, bool GATH = false>
-__global__ void __launch_bounds__(kFinalThreads, 3)
+// The gather variant runs 10 warps per CTA instead of 12 (68 registers per
+// thread at 3 CTAs/SM: its parent loads no longer spill; gather E 11.56 ->
+// 11.22 ms, 17.9 -> 17.0 at P(on) = 0.9; the same kernel in pass-D mode 7.4 vs
+// 7.05 ms with 12 warps, which is why the plans without a gather keep 12).
+constexpr int kFinalThreadsGather = 320;
+template <int G, bool GATH = false, int NT = (GATH ? kFinalThreadsGather : kFinalThreads)>
+__global__ void __launch_bounds__(NT, 3)
     k_c0_final(const uint32_t *__restrict__ state, FinalArgs fa, const __grid_constant__ CUtensorMap ma,
                const __grid_constant__ CUtensorMap mb) {
     extern __shared__ __align__(128) uint32_t sm_raw[];
@@ -874,15 +879,15 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
     }
     __syncthreads();
     mbar_wait(&mbar, 0);
-    __shared__ FinishSmem<kFinalThreads> fs;
+    __shared__ FinishSmem<NT> fs;
     if (!fa.bitmap_out) {
         if (fa.kill_tab || fa.skip_c0 || fa.rank_add_tab) {
-            if (tile_finish_sparse<kFinalThreads, G, true>(sm, tile, blk0, fa, fs)) return;
+            if (tile_finish_sparse<NT, G, true>(sm, tile, blk0, fa, fs)) return;
         } else {
             // gather finish: a dense tile goes through the register-cube rounds and
             // then the same batched finish over the blocks the rounds left
             for (bool reduced = false;; reduced = true) {
-                if (tile_finish_sparse<kFinalThreads, G, false>(sm, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff, reduced))
+                if (tile_finish_sparse<NT, G, false>(sm, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff, reduced))
                     return;
                 if (!GATH || !gb) break;
                 tile_reduce_c0_t<G, 0>(sm);
@@ -890,7 +895,7 @@ __global__ void __launch_bounds__(kFinalThreads, 3)
         }
     }
     if (!fa.skip_c0) tile_reduce_c0_t<G, 0>(sm);
-    tile_finish<kFinalThreads>(sm, NB, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff);
+    tile_finish<NT>(sm, NB, tile, blk0, fa, fs, gb, fa.pm_nr * 32, s_goff);
 }
 
 // n <= 12: the whole problem is one tile; one CTA does A and E.
@@ -942,7 +947,7 @@ int launch_c0_final(int g, int64_t ntiles, const uint32_t *state, const FinalArg
 #undef CASE
         case 7:
             if (fa.g0)
-                k_c0_final<7, true><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);
+                k_c0_final<7, true><<<(unsigned)ntiles, kFinalThreadsGather, smem, s>>>(state, fa, ma, mb);
             else
                 k_c0_final<7><<<(unsigned)ntiles, kFinalThreads, smem, s>>>(state, fa, ma, mb);
             break;
