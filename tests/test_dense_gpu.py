@@ -388,6 +388,45 @@ class TestAsyncAndGraph:
             with pytest.raises(RuntimeError):
                 g.ranks()
 
+    @pytest.mark.slow
+    def test_graph_n24_finish_follows_the_data(self, pkg, golden):
+        """One captured graph of the n=24 plan holds both ways to finish a
+        state; which one runs is decided on the device at every replay
+        (DESIGN.md 3c). Captured on a dense table (pass D), replayed on it,
+        then on BASELINE config 4 refilled in place (gather finish): each
+        replay equals the direct call / the reference's count and hash."""
+        import ctypes
+
+        import torch
+        from paper_2302_10083_b200 import _lib, device
+
+        L = _lib.load()
+
+        def gathered():
+            nzb, tot, g = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int(0)
+            _lib.check(L.dqmc_last_gather(ctypes.byref(nzb), ctypes.byref(tot), ctypes.byref(g)))
+            return g.value
+
+        n = 24
+        v = device.gen3_device(n, 0.99, 0.0, 4)
+        ref, cnt = device.dense_prime_ranks_device(v, n)
+        want = rsha(ref.cpu().numpy())
+        del ref
+        torch.cuda.empty_cache()
+        g = device.PrimesGraph(v, n, headroom=1.0)
+        g.replay()
+        r = g.ranks()
+        assert r.numel() == cnt and rsha(r.cpu().numpy()) == want
+        assert gathered() == 0
+        _lib.check(L.dqmc_gen3_device(v.data_ptr(), n, 0.75, 0.05, 3, torch.cuda.current_stream().cuda_stream))
+        g.replay()
+        r = g.ranks()
+        g4 = golden["configs"]["4"]
+        assert r.numel() == g4["primes"] and rsha(r.cpu().numpy())[:16] == g4["ranks_sha256_prefix"]
+        assert gathered() == 1
+        del g, r
+        torch.cuda.empty_cache()
+
 
 class TestJobStream:
     """dqmc_submit_* / dqmc_collect: three calls in flight, results identical to
