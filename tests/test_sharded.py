@@ -115,6 +115,33 @@ class CpuOps:
 # the plan
 
 
+def test_star_block_is_the_merge_of_the_anded_tables(oracle_mod, gen_mod):
+    """MERGE is an AND-homomorphism on truth tables: a cube is an implicant of
+    f0 AND f1 iff it is one of both. So the '*' block of the top variable
+    (dense.py:174-212, u = s & t) equals the merged array of the table
+    f0 & f1 on its own, and blocks 0/1 those of f0/f1: a rank can build any
+    top block from ANDed 2^(n-k)-bit tables instead of exchanging
+    3^(n-k)-bit arrays."""
+    MERGE = 0
+    for n, seed in ((9, 1), (12, 2), (14, 3)):
+        words = gen_mod.random_words(n, 0.8, seed)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: 1 << n]
+        f0, f1 = bits[: 1 << (n - 1)], bits[1 << (n - 1):]
+        full = oracle_mod.OracleState(words, n)
+        full.run_pass(MERGE)
+        top = full.words.reshape(3, -1)  # the top variable is the slowest block digit: blocks 0, 1, *
+
+        def merged(b):
+            w = np.packbits(np.pad(b, (0, (-len(b)) % 64)), bitorder="little").view(np.uint64)
+            st = oracle_mod.OracleState(w, n - 1)
+            st.run_pass(MERGE)
+            return st.words
+
+        assert np.array_equal(top[0], merged(f0))
+        assert np.array_equal(top[1], merged(f1))
+        assert np.array_equal(top[2], merged(f0 & f1))
+
+
 class TestPlan:
     @pytest.mark.parametrize("n,k", [(12, 1), (13, 2), (14, 3), (24, 3), (27, 3), (24, 1)])
     def test_ownership_rules(self, n, k):
