@@ -357,7 +357,7 @@ struct Plan {
 // are kNzWords words. REDUCE only clears bits, so a zero flag is exact for D
 // and E.
 constexpr int kNzWords = 24;
-constexpr int kGatherPermille = 500;  // default dqmc_gather_threshold
+constexpr int kGatherPermille = 600;  // default dqmc_gather_threshold
 // Flag layout in g_eng.nzflags (npiece = pieces per C0 tile, nr = 3^6 group-0
 // rows): nz_b [npiece][3 boxes of 243 rows][kNzWords] (pass D's items (x, u)
 // per box), nz_e [nr][kNzWords] (pass E's tiles (u, l)), then a zero page of
